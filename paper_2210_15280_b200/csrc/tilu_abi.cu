@@ -1,0 +1,437 @@
+// C ABI of libtilu (include/tilu.h): plan construction and the stream-ordered drivers that
+// chain the kernels of one smoothing step.  No exceptions cross the boundary; every entry
+// point returns a status code and records a thread-local message.
+#include <algorithm>
+#include <cstdarg>
+#include <map>
+#include <mutex>
+#include <string>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "tilu.h"
+#include "tilu_common.cuh"
+#include "tilu_plan.cuh"
+
+namespace tilu {
+void launch_seed(const PlanDev &P, const double *lcoefs, const double *dcoefs, double *seedF, double *seedB,
+                 cudaStream_t s);
+void launch_seed_op(const PlanDev &P, const double *acoefs, int ky1, int kz1, double *seedA, cudaStream_t s);
+void launch_residual(const PlanDev &P, bool exact, const double *u, const double *f, double *w, double *part,
+                     int ntets, bool apply_only, cudaStream_t s);
+bool launch_residual_sop(const PlanDev &P, const double *u, const double *f, double *w, double *part, int ntets,
+                         cudaStream_t s);
+void launch_reduce_rows(const double *part, int nrows, double *out, int ntets, cudaStream_t s);
+bool launch_simple_solve(const PlanDev &P, bool exact, bool stored, double *w, double *state, double *u, int ntets,
+                         int which, cudaStream_t s);
+// plane-layout fast path (tilu_plane.cu)
+void prof_begin(cudaStream_t s);
+void prof_end(const char *name, cudaStream_t s);
+bool plane_supported(const tilu_plan *plan);
+int plane_sweep(const tilu_plan *plan, double *u, const double *f, int ntets, int sweeps, double *rnorm2,
+                cudaStream_t s, int *launches);
+}  // namespace tilu
+
+using namespace tilu;
+
+// ---- per-kernel event timing (tilu_profile_*) ------------------------------------------------
+namespace {
+struct ProfRec {
+    const char *name;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof_pending;
+std::map<std::string, std::pair<int, double>> g_prof_acc;
+thread_local cudaEvent_t g_prof_open = nullptr;
+}  // namespace
+
+namespace tilu {
+void prof_begin(cudaStream_t s)
+{
+    if (!g_prof_on) return;
+    cudaEventCreate(&g_prof_open);
+    cudaEventRecord(g_prof_open, s);
+}
+void prof_end(const char *name, cudaStream_t s)
+{
+    if (!g_prof_on || !g_prof_open) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_pending.push_back({name, g_prof_open, b});
+    g_prof_open = nullptr;
+}
+}  // namespace tilu
+
+namespace {
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+int fail(int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int check_cuda(const char *what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(TILU_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return TILU_OK;
+}
+
+template <class T>
+int dev_upload(tilu_plan *p, T **dst, const T *src, size_t count)
+{
+    *dst = nullptr;
+    if (count == 0) return TILU_OK;
+    if (p->nallocs >= (int)(sizeof(p->allocs) / sizeof(p->allocs[0]))) return fail(TILU_ENOMEM, "too many plan buffers");
+    void *d = nullptr;
+    if (cudaMalloc(&d, count * sizeof(T)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(TILU_ENOMEM, "cudaMalloc(%zu bytes) failed", count * sizeof(T));
+    }
+    p->allocs[p->nallocs++] = d;
+    if (src && cudaMemcpy(d, src, count * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail(TILU_ECUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+    *dst = static_cast<T *>(d);
+    return TILU_OK;
+}
+
+struct Scratch {
+    cudaStream_t s;
+    std::vector<void *> bufs;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    ~Scratch()
+    {
+        for (void *b : bufs) cudaFreeAsync(b, s);
+    }
+    double *get(size_t count)
+    {
+        void *d = nullptr;
+        if (cudaMallocAsync(&d, count * sizeof(double), s) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        bufs.push_back(d);
+        return static_cast<double *>(d);
+    }
+};
+
+bool valid_plan(const tilu_plan_t *p) { return p != nullptr && p->dev.n > 0; }
+}  // namespace
+
+extern "C" {
+
+void tilu_profile_enable(int on) { g_prof_on = on != 0; }
+
+void tilu_profile_reset(void)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto &r : g_prof_pending) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof_pending.clear();
+    g_prof_acc.clear();
+}
+
+int tilu_profile_read(char *names, int *counts, double *ms, int cap)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto &r : g_prof_pending) {
+        float t = 0.f;
+        cudaEventSynchronize(r.b);
+        cudaEventElapsedTime(&t, r.a, r.b);
+        auto &e = g_prof_acc[r.name];
+        e.first += 1;
+        e.second += t;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof_pending.clear();
+    int i = 0;
+    for (auto &kv : g_prof_acc) {
+        if (i >= cap) break;
+        std::snprintf(names + 64 * i, 64, "%s", kv.first.c_str());
+        counts[i] = kv.second.first;
+        ms[i] = kv.second.second;
+        ++i;
+    }
+    return (int)g_prof_acc.size();
+}
+
+const char *tilu_last_error(void) { return g_err; }
+int tilu_version(void) { return 100; }
+int tilu_last_launch_count(void) { return g_launches; }
+int64_t tilu_plan_grid_size(const tilu_plan_t *p) { return p ? p->dev.grid : -1; }
+int64_t tilu_plan_interior_size(const tilu_plan_t *p) { return p ? p->interior : -1; }
+
+void tilu_plan_destroy(tilu_plan_t *p)
+{
+    if (!p) return;
+    for (int i = 0; i < p->nallocs; ++i) cudaFree(p->allocs[i]);
+    delete p;
+}
+
+int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
+{
+    g_launches = 0;
+    if (!d || !out) return fail(TILU_EINVAL, "null descriptor / output");
+    *out = nullptr;
+    if (d->level < 2 || d->level > 10) return fail(TILU_EINVAL, "level %d outside 2..10", d->level);
+    if (d->kx1 < 1 || d->ky1 < 1 || d->kz1 < 1) return fail(TILU_EINVAL, "coefficient extents must be >= 1");
+    if (d->kx1 > 9 || d->ky1 > 16 || d->kz1 > 16) return fail(TILU_EUNSUPPORTED, "kx+1 <= 9 (and ky+1, kz+1 <= 16) supported");
+    if (d->variant != TILU_VARIANT_V1 && d->variant != TILU_VARIANT_V2) return fail(TILU_EINVAL, "variant must be V1 or V2");
+    if (!d->lcoefs || !d->dcoefs) return fail(TILU_EINVAL, "lcoefs / dcoefs required");
+    if (d->acoefs && (d->akx1 < 1 || d->akx1 > 9 || d->aky1 < 1 || d->akz1 < 1 || d->aky1 > 16 || d->akz1 > 16))
+        return fail(TILU_EUNSUPPORTED, "operator surrogate extents unsupported");
+    const int n = 1 << d->level;
+    if (n < 4) return fail(TILU_EINVAL, "level too small");
+
+    tilu_plan *p = new (std::nothrow) tilu_plan();
+    if (!p) return fail(TILU_ENOMEM, "host allocation failed");
+    std::memset(p, 0, sizeof(*p));
+    p->flags = d->flags;
+    PlanDev &P = p->dev;
+    P.level = d->level;
+    P.n = n;
+    P.grid = num_points(n);
+    P.kx1 = d->kx1;
+    P.ky1 = d->ky1;
+    P.kz1 = d->kz1;
+    P.variant = d->variant;
+    P.h = 1.0 / n;
+    P.tmin = 6;
+    P.tmax = 3 * n - 6;
+    p->interior = num_points(n - 4);
+
+    // rows in (z, y) order
+    std::vector<RowInfo> rows;
+    std::vector<int64_t> rowbase;
+    for (int z = 1; z <= n - 3; ++z)
+        for (int y = 1; y <= n - 2 - z; ++y) {
+            rows.push_back({z, y, n - 1 - z - y, 1 + 2 * y + 3 * z});
+            rowbase.push_back(row_offset(n, z, y));
+        }
+    P.nrows = (int)rows.size();
+    p->nband = 0;
+
+    int rc = TILU_OK;
+    std::vector<int> bandoff;
+    if (d->variant == TILU_VARIANT_V1) {
+        if (!d->band_ranks || !d->store_rows || d->nband <= 0) {
+            tilu_plan_destroy(p);
+            return fail(TILU_EINVAL, "V1 needs band_ranks and store_rows");
+        }
+        // The reference looks rows up by binary search in the sorted band ranks (_kernels.py:27-36);
+        // accept exactly the canonical band set (surrogate.py:223-229) so per-row offsets are equivalent.
+        int64_t k = 0;
+        bool ok = true;
+        for (size_t r = 0; r < rows.size() && ok; ++r) {
+            const RowInfo &ri = rows[r];
+            bandoff.push_back((int)k);
+            for (int x = 1; x <= ri.xe; ++x) {
+                const bool band = ri.z == 1 || ri.y == 1 || x == 1 || x == ri.xe;
+                if (!band) continue;
+                if (k >= d->nband || d->band_ranks[k] != rowbase[r] + x) { ok = false; break; }
+                ++k;
+            }
+        }
+        if (!ok || k != d->nband) {
+            tilu_plan_destroy(p);
+            return fail(TILU_EINVAL, "band_ranks is not the canonical boundary band of level %d", d->level);
+        }
+        p->nband = d->nband;
+    }
+
+    RowInfo *drows = nullptr;
+    int64_t *drowbase = nullptr;
+    int *dbandoff = nullptr;
+    double *dstore = nullptr, *dl = nullptr, *dd = nullptr, *dseedF = nullptr, *dseedB = nullptr, *darow = nullptr;
+    double *dacoefs = nullptr, *dseedA = nullptr, *dfactors = nullptr;
+    const int K = d->kx1;
+    if ((rc = dev_upload(p, &drows, rows.data(), rows.size())) ||
+        (rc = dev_upload(p, &drowbase, rowbase.data(), rowbase.size())) ||
+        (rc = dev_upload(p, &dl, d->lcoefs, (size_t)7 * K * d->ky1 * d->kz1)) ||
+        (rc = dev_upload(p, &dd, d->dcoefs, (size_t)K * d->ky1 * d->kz1)) ||
+        (rc = dev_upload(p, &dseedF, (const double *)nullptr, (size_t)P.nrows * 7 * K)) ||
+        (rc = dev_upload(p, &dseedB, (const double *)nullptr, (size_t)P.nrows * 8 * K))) {
+        tilu_plan_destroy(p);
+        return rc;
+    }
+    if (d->variant == TILU_VARIANT_V1 &&
+        ((rc = dev_upload(p, &dbandoff, bandoff.data(), bandoff.size())) ||
+         (rc = dev_upload(p, &dstore, d->store_rows, (size_t)d->nband * 9)))) {
+        tilu_plan_destroy(p);
+        return rc;
+    }
+    if (d->arow && (rc = dev_upload(p, &darow, d->arow, 15))) {
+        tilu_plan_destroy(p);
+        return rc;
+    }
+    if (d->factors && (rc = dev_upload(p, &dfactors, d->factors, (size_t)P.grid * 9))) {
+        tilu_plan_destroy(p);
+        return rc;
+    }
+    P.rows = drows;
+    P.rowbase = drowbase;
+    P.bandoff = dbandoff;
+    P.store = dstore;
+    P.seedF = dseedF;
+    P.seedB = dseedB;
+    P.arow = darow;
+    P.arows = d->arow ? nullptr : d->arows_dev;
+    P.factors = dfactors;
+    if (d->acoefs) {
+        P.akx1 = d->akx1;
+        p->ky1a = d->aky1;
+        p->kz1a = d->akz1;
+        if ((rc = dev_upload(p, &dacoefs, d->acoefs, (size_t)15 * d->akx1 * d->aky1 * d->akz1)) ||
+            (rc = dev_upload(p, &dseedA, (const double *)nullptr, (size_t)P.nrows * 15 * d->akx1))) {
+            tilu_plan_destroy(p);
+            return rc;
+        }
+        P.seedA = dseedA;
+    }
+    launch_seed(P, dl, dd, dseedF, dseedB, 0);
+    if (d->acoefs) launch_seed_op(P, dacoefs, d->aky1, d->akz1, dseedA, 0);
+    if (cudaDeviceSynchronize() != cudaSuccess || (rc = check_cuda("seed tables"))) {
+        rc = fail(TILU_ECUDA, "seed kernel failed: %s", cudaGetErrorString(cudaGetLastError()));
+        tilu_plan_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return TILU_OK;
+}
+
+static int solve_common(const tilu_plan_t *p, double *w, int ntets, int which, bool stored, void *stream)
+{
+    g_launches = 0;
+    if (!valid_plan(p) || !w || ntets < 1) return fail(TILU_EINVAL, "invalid plan / vector / ntets");
+    if (stored && !p->dev.factors) return fail(TILU_EINVAL, "plan has no stored factors");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Scratch sc(s);
+    double *state = nullptr;
+    if (!stored && !(state = sc.get((size_t)ntets * p->dev.nrows * 8 * p->dev.kx1)))
+        return fail(TILU_ENOMEM, "scratch allocation failed");
+    prof_begin(s);
+    const bool ok = launch_simple_solve(p->dev, !(p->flags & TILU_FAST), stored, w, state, nullptr, ntets, which, s);
+    prof_end(stored ? "stored_solve" : "simple_solve", s);
+    if (!ok) return fail(TILU_EUNSUPPORTED, "kx+1 = %d not compiled", p->dev.kx1);
+    g_launches = (which == 3) ? 2 : 1;
+    return check_cuda("solve");
+}
+
+int tilu_solve_into(const tilu_plan_t *p, double *w, int ntets, void *stream) { return solve_common(p, w, ntets, 3, false, stream); }
+int tilu_surrogate_forward(const tilu_plan_t *p, double *w, int ntets, void *stream) { return solve_common(p, w, ntets, 1, false, stream); }
+int tilu_surrogate_backward(const tilu_plan_t *p, double *w, int ntets, void *stream) { return solve_common(p, w, ntets, 2, false, stream); }
+int tilu_stored_solve_into(const tilu_plan_t *p, double *w, int ntets, void *stream) { return solve_common(p, w, ntets, 3, true, stream); }
+
+static int residual_into(const tilu_plan_t *p, const double *u, const double *f, double *w, int ntets, double *rnorm2,
+                         double *part, cudaStream_t s)
+{
+    const PlanDev &P = p->dev;
+    if (P.seedA) {
+        prof_begin(s);
+        const bool ok = launch_residual_sop(P, u, f, w, part, ntets, s);
+        prof_end("residual_sop", s);
+        if (!ok) return fail(TILU_EUNSUPPORTED, "operator surrogate degree");
+    } else if (P.arow || P.arows) {
+        prof_begin(s);
+        launch_residual(P, !(p->flags & TILU_FAST), u, f, w, part, ntets, false, s);
+        prof_end("residual", s);
+    } else {
+        return fail(TILU_EINVAL, "plan has no operator (arow / arows_dev / acoefs)");
+    }
+    ++g_launches;
+    if (rnorm2) {
+        prof_begin(s);
+        launch_reduce_rows(part, P.nrows, rnorm2, ntets, s);
+        prof_end("reduce_rows", s);
+        ++g_launches;
+    }
+    return TILU_OK;
+}
+
+int tilu_residual(const tilu_plan_t *p, const double *u, const double *f, double *w, int ntets, double *rnorm2,
+                  void *stream)
+{
+    g_launches = 0;
+    if (!valid_plan(p) || !u || !f || !w || ntets < 1) return fail(TILU_EINVAL, "invalid arguments");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Scratch sc(s);
+    double *part = rnorm2 ? sc.get((size_t)ntets * p->dev.nrows) : nullptr;
+    if (rnorm2 && !part) return fail(TILU_ENOMEM, "scratch allocation failed");
+    int rc = residual_into(p, u, f, w, ntets, rnorm2, part, s);
+    return rc ? rc : check_cuda("residual");
+}
+
+int tilu_stencil_apply(const tilu_plan_t *p, const double *u, double *out, int ntets, void *stream)
+{
+    g_launches = 0;
+    if (!valid_plan(p) || !u || !out || ntets < 1) return fail(TILU_EINVAL, "invalid arguments");
+    if (!p->dev.arow && !p->dev.arows) return fail(TILU_EINVAL, "plan has no stencil rows");
+    launch_residual(p->dev, true, u, nullptr, out, nullptr, ntets, true, static_cast<cudaStream_t>(stream));
+    g_launches = 1;
+    return check_cuda("stencil_apply");
+}
+
+static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int ntets, int sweeps, double *rnorm2,
+                        bool stored, void *stream)
+{
+    g_launches = 0;
+    if (!valid_plan(p) || !u || !f || ntets < 1 || sweeps < 0) return fail(TILU_EINVAL, "invalid arguments");
+    if (stored && !p->dev.factors) return fail(TILU_EINVAL, "plan has no stored factors");
+    if (sweeps == 0) return TILU_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!stored && !(p->flags & TILU_SCHED_SIMPLE) && plane_supported(p)) {
+        int launches = 0;
+        int rc = plane_sweep(p, u, f, ntets, sweeps, rnorm2, s, &launches);
+        g_launches = launches;
+        if (rc != TILU_OK) return fail(rc, "plane sweep failed: %s", cudaGetErrorString(cudaGetLastError()));
+        return check_cuda("plane sweep");
+    }
+    const PlanDev &P = p->dev;
+    Scratch sc(s);
+    double *w = sc.get((size_t)ntets * P.grid);
+    double *state = stored ? nullptr : sc.get((size_t)ntets * P.nrows * 8 * P.kx1);
+    double *part = sc.get((size_t)ntets * P.nrows);
+    if (!w || (!stored && !state) || !part) return fail(TILU_ENOMEM, "scratch allocation failed");
+    cudaMemsetAsync(w, 0, sizeof(double) * ntets * P.grid, s);
+    const bool exact = !(p->flags & TILU_FAST);
+    for (int k = 0; k < sweeps; ++k) {
+        int rc = residual_into(p, u, f, w, ntets, rnorm2 ? rnorm2 + (int64_t)k * ntets : nullptr, part, s);
+        if (rc) return rc;
+        prof_begin(s);
+        bool ok = launch_simple_solve(P, exact, stored, w, state, u, ntets, 1, s);
+        prof_end(stored ? "stored_fwd" : "simple_fwd", s);
+        prof_begin(s);
+        ok = ok && launch_simple_solve(P, exact, stored, w, state, u, ntets, 2, s);
+        prof_end(stored ? "stored_bwd" : "simple_bwd", s);
+        if (!ok) return fail(TILU_EUNSUPPORTED, "kx+1 = %d not compiled", P.kx1);
+        g_launches += 2;
+    }
+    return check_cuda("sweep");
+}
+
+int tilu_sweep(const tilu_plan_t *p, double *u, const double *f, int ntets, int sweeps, double *rnorm2, void *stream)
+{
+    return sweep_common(p, u, f, ntets, sweeps, rnorm2, false, stream);
+}
+
+int tilu_stored_sweep(const tilu_plan_t *p, double *u, const double *f, int ntets, int sweeps, double *rnorm2,
+                      void *stream)
+{
+    return sweep_common(p, u, f, ntets, sweeps, rnorm2, true, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,48 @@
+// Device-side plan layout shared by all kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tilu.h"
+
+namespace tilu {
+
+// Per-row metadata, rows in (z, y) lexicographic order (row_id()).
+struct RowInfo {
+    int z, y, xe, t0;  // t0 = first hyperplane step of the row: 1 + 2y + 3z (x = 1)
+};
+
+// POD view passed by value to kernels.
+struct PlanDev {
+    int level, n;
+    int64_t grid;
+    int nrows;
+    int kx1, ky1, kz1;
+    int variant;  // 1 = V1, 2 = V2
+    double h;
+    int tmin, tmax;                  // hyperplane t = x + 2y + 3z over the interior
+    const RowInfo *rows;             // [nrows]
+    const int64_t *rowbase;          // [nrows] rank of (0, y, z)
+    const int *bandoff;              // [nrows] first band entry of the row (V1)
+    const double *store;             // [nband][9] (V1)
+    const double *seedF;             // [nrows][7][kx1]  forward-difference tables, forward pass
+    const double *seedB;             // [nrows][8][kx1]  backward pass: 7 shifted L + 1/D
+    const double *arow;              // [15] constant stencil or nullptr
+    const double *arows;             // [grid][15] per-point rows or nullptr
+    const double *seedA;             // [nrows][15][akx1] operator-surrogate tables or nullptr
+    int akx1;
+    const double *factors;           // [grid][9] stored ILU rows or nullptr
+};
+
+}  // namespace tilu
+
+struct tilu_plan {
+    tilu::PlanDev dev;
+    int flags;
+    int64_t interior;
+    int64_t nband;
+    int ky1a, kz1a;
+    // owned device allocations
+    void *allocs[16];
+    int nallocs;
+};

@@ -1,0 +1,126 @@
+"""Macro-tet partitioning across GPUs (config 4: 384 Kuhn macro-tets on 1-8 B200).
+
+Macro-tets with Dirichlet data on every macro-face are independent units: the
+reference's cell stage is block-Jacobi across cells (multigrid.py:419-429), so the
+sweep itself needs no halo exchange.  Each rank (one process per GPU) owns a
+contiguous block of tets; the only collective is the per-sweep residual-norm
+allreduce (one fp64 per sweep, NCCL over NVLink/NVSwitch), enqueued on a side
+stream so it overlaps the next sweep.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+from . import lattice
+from .smoother import SmootherConfig, SurrogateILUSmoother
+from .stencil import CoefficientField, stencil_source
+
+try:
+    import torch
+    import torch.distributed as dist
+except ImportError:  # pragma: no cover
+    torch = dist = None
+
+
+def partition(ntets: int, world_size: int) -> list[range]:
+    """Contiguous blocks, sizes differing by at most one (equal DoF per tet -> balanced)."""
+    if world_size < 1 or ntets < 0:
+        raise ValueError("world_size >= 1 and ntets >= 0 required")
+    base, extra = divmod(ntets, world_size)
+    out, start = [], 0
+    for r in range(world_size):
+        size = base + (1 if r < extra else 0)
+        out.append(range(start, start + size))
+        start += size
+    return out
+
+
+def group_by_operator(rows: list[np.ndarray]) -> list[list[int]]:
+    """Indices of tets whose operator rows are bitwise identical share one surrogate."""
+    groups: dict[bytes, list[int]] = {}
+    for i, r in enumerate(rows):
+        groups.setdefault(hashlib.sha1(np.ascontiguousarray(r).tobytes()).digest(), []).append(i)
+    return list(groups.values())
+
+
+def allreduce_norms(local: "torch.Tensor", group=None) -> "torch.Tensor":
+    """Sum of per-rank residual norm^2 (in place); a no-op on one rank."""
+    if dist is not None and dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(local, op=dist.ReduceOp.SUM, group=group)
+    return local
+
+
+class MacroMeshSmoother:
+    """Smoother over this rank's share of a macro-mesh of independent macro-tets."""
+
+    def __init__(self, tets: list[np.ndarray], level: int, coeff: CoefficientField | None = None,
+                 degrees=(6, 6, 6), variant: str = "v1", rank: int = 0, world_size: int = 1, group=None,
+                 fast: bool = False, simple: bool = False):
+        self.level = level
+        self.grid = lattice.grid_size(level)
+        self.ntets_global = len(tets)
+        self.local = partition(len(tets), world_size)[rank]
+        self.group = group
+        coeff = coeff or CoefficientField.constant(1.0)
+        sources = [stencil_source(tets[i], level, coeff) for i in self.local]
+        self.groups = group_by_operator([s.data for s in sources])
+        self.smoothers = [SurrogateILUSmoother(sources[g[0]], level, SmootherConfig(
+            "surrogate_ilu", tuple(degrees), variant), fast=fast, simple=simple) for g in self.groups]
+        self._side = None
+        self.launches = 0   # kernels enqueued by apply() so far (bench accounting)
+
+    @property
+    def ntets_local(self) -> int:
+        return len(self.local)
+
+    def apply(self, u: "torch.Tensor", f: "torch.Tensor", sweeps: int = 1, residual_norms: bool = True):
+        """u, f: this rank's tets [ntets_local, grid] (CUDA fp64).  Returns the global
+        ||f - A u||^2 before each sweep ([sweeps], summed over all ranks) if requested."""
+        if u.shape != (self.ntets_local, self.grid):
+            raise ValueError(f"u must be [{self.ntets_local}, {self.grid}]")
+        norms = torch.zeros(sweeps, dtype=torch.float64, device=u.device) if residual_norms else None
+        if self._side is None and residual_norms:
+            self._side = torch.cuda.Stream(device=u.device)
+        views = []
+        for g, sm in zip(self.groups, self.smoothers):
+            contiguous = g == list(range(g[0], g[0] + len(g)))
+            views.append((sm, g, contiguous))
+        for k in range(sweeps):
+            for sm, g, contiguous in views:
+                if contiguous:
+                    rn = sm.apply(u[g[0]:g[0] + len(g)], f[g[0]:g[0] + len(g)], 1,
+                                  residual_norms=residual_norms)
+                else:
+                    idx = torch.as_tensor(g, device=u.device)
+                    ug = u.index_select(0, idx).contiguous()
+                    rn = sm.apply(ug, f.index_select(0, idx).contiguous(), 1, residual_norms=residual_norms)
+                    u.index_copy_(0, idx, ug)
+                self.launches += sm.plan.last_launch_count()
+                if residual_norms:
+                    norms[k] += rn.sum()
+            if residual_norms:
+                # overlap the collective with the next sweep: side stream waits for this sweep only
+                ev = torch.cuda.Event()
+                ev.record()
+                with torch.cuda.stream(self._side):
+                    self._side.wait_event(ev)
+                    allreduce_norms(norms[k:k + 1], self.group)
+        if residual_norms:
+            torch.cuda.current_stream().wait_stream(self._side)
+        return norms
+
+    def apply_host(self, u_host: "torch.Tensor", f_host: "torch.Tensor", sweeps: int = 1,
+                   residual_norms: bool = True):
+        """End-to-end call on (pinned) host tensors: H2D of u and f, ``sweeps`` sweeps, D2H of u
+        (in place) and of the global norms.  Returns the norms (host tensor) or None."""
+        dev = torch.device("cuda", torch.cuda.current_device())
+        u = u_host.to(dev, non_blocking=True)
+        f = f_host.to(dev, non_blocking=True)
+        norms = self.apply(u, f, sweeps, residual_norms)
+        u_host.copy_(u, non_blocking=True)
+        out = norms.to("cpu", non_blocking=True) if residual_norms else None
+        torch.cuda.current_stream().synchronize()
+        return out

@@ -1,0 +1,214 @@
+"""GPU parity: the CUDA path (through the C ABI) against the C oracle / golden vectors.
+
+Bar: bitwise in the default exact mode (same operation order, no FMA), <= 1e-12 max
+relative error per sweep in fast (FMA) mode, asymptotic rate to 3 significant digits.
+"""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from paper_2210_15280_b200 import (DevicePlan, SurrogateILUSmoother, build_surrogate_ilu,  # noqa: E402
+                                   lattice)
+from paper_2210_15280_b200 import fitting as F  # noqa: E402
+from paper_2210_15280_b200 import stencil as S  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "cfg*.npz")))
+DEV = "cuda"
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name + ".npz"))
+
+
+def plan_of(d, fast=False, simple=False, **op):
+    return DevicePlan(int(d["level"]), d["lcoefs"], d["dcoefs"], str(d["variant"]), d["band_ranks"],
+                      d["store_rows"], fast=fast, simple=simple, **op)
+
+
+def op_of(d):
+    a = d["arows"]
+    return {"arow": a[0]} if a.shape[0] == 1 else {"arows": a}
+
+
+def cuda(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device=DEV)
+
+
+def relerr(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_solve_into_bitwise_vs_reference(name):
+    d = load(name)
+    if "solve_in" not in d:
+        pytest.skip("no solve pin")
+    w = cuda(d["solve_in"])
+    plan_of(d).solve_into(w)
+    assert np.array_equal(w.cpu().numpy(), d["solve_out"])
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("simple", [True, False])
+def test_sweeps_bitwise_vs_reference(name, simple):
+    d = load(name)
+    k = int(d["sweeps"])
+    p = plan_of(d, simple=simple, **op_of(d))
+    u, f = cuda(d["u0"]), cuda(d["f"])
+    rn = p.sweep(u, f, 1, norms=True)
+    assert np.array_equal(u.cpu().numpy(), d["u_after_1"])
+    rn2 = p.sweep(u, f, k - 1, norms=True)
+    assert np.array_equal(u.cpu().numpy(), d[f"u_after_{k}"])
+    norms = np.concatenate([rn.cpu().numpy().ravel(), rn2.cpu().numpy().ravel()])
+    np.testing.assert_allclose(norms, d["rnorm2"], rtol=1e-12, atol=1e-300)
+
+
+@pytest.mark.parametrize("name", ["cfg1_L5_v1", "cfg2_L4_v1"])
+def test_stored_ilu_bitwise(name):
+    d = load(name)
+    p = DevicePlan(int(d["level"]), np.zeros((7, 1, 1, 1)), np.zeros(1), "v2", factors=d["factors"], **op_of(d))
+    w = cuda(d["ilu_solve_in"])
+    p.stored_solve_into(w)
+    assert np.array_equal(w.cpu().numpy(), d["ilu_solve_out"])
+    u, f = cuda(d["u0"]), cuda(d["f"])
+    p.sweep(u, f, int(d["sweeps"]), stored=True)
+    assert np.array_equal(u.cpu().numpy(), d["ilu_u_final"])
+
+
+@pytest.mark.parametrize("name", ["nddf_L3", "nddf_L4", "nddf_L5"])
+@pytest.mark.parametrize("variant", ["v1", "v2"])
+def test_random_shapes_bitwise(name, variant):
+    d = load(name)
+    L = int(d["level"])
+    for i, _ in enumerate(d["shapes"]):
+        p = DevicePlan(L, d[f"s{i}_lcoefs"], d[f"s{i}_dcoefs"], variant, d["band_ranks"], d[f"s{i}_store"])
+        w = cuda(d[f"s{i}_w0"])
+        p.forward(w)
+        assert np.array_equal(w.cpu().numpy(), d[f"s{i}_{variant}_fwd"])
+        p.backward(w)
+        assert np.array_equal(w.cpu().numpy(), d[f"s{i}_{variant}_solve"])
+
+
+def test_stencil_apply_and_operator_surrogate_bitwise():
+    d = load("kernels_L4")
+    z = np.zeros((7, 1, 1, 1))
+    p = DevicePlan(4, z, np.zeros(1), "v2", arows=d["arows"])
+    assert np.array_equal(p.stencil_apply(cuda(d["u"])).cpu().numpy(), d["stencil_out"])
+    p1 = DevicePlan(4, z, np.zeros(1), "v2", arow=d["arow1"][0])
+    assert np.array_equal(p1.stencil_apply(cuda(d["u"])).cpu().numpy(), d["stencil_out1"])
+    ps = DevicePlan(4, z, np.zeros(1), "v2", acoefs=d["acoefs"])
+    w = ps.residual(cuda(d["u"]), cuda(d["f"]))
+    assert np.array_equal(w.cpu().numpy(), d["sres_out"])
+    s = load("sop_L4")
+    pp = plan_of(s, acoefs=s["acoefs"])
+    u = torch.zeros(len(s["f"]), dtype=torch.float64, device=DEV)
+    pp.sweep(u, cuda(s["f"]), 3)
+    assert np.array_equal(u.cpu().numpy(), s["u_after_3"])
+
+
+def _oracle_case(level, q, variant="v1", coeff=None, verts=None, seed=0):
+    verts = lattice.unit_tet() if verts is None else verts
+    src = S.stencil_source(verts, level, coeff or S.CoefficientField.constant(1.0))
+    fit = F.fit_surrogate_ilu(src, level, (q, q, q), variant)
+    mask = lattice.interior_mask(level)
+    u0 = np.zeros(lattice.grid_size(level))
+    u0[mask] = np.random.default_rng(seed).uniform(-1, 1, int(mask.sum()))
+    return src, fit, u0
+
+
+@pytest.mark.parametrize("level,q,variant", [(2, 3, "v1"), (3, 2, "v2"), (6, 4, "v1"), (6, 6, "v2"), (7, 6, "v1")])
+@pytest.mark.parametrize("simple", [True, False])
+def test_larger_levels_bitwise_vs_oracle(level, q, variant, simple):
+    src, fit, u0 = _oracle_case(level, q, variant)
+    f = np.zeros_like(u0)
+    ref = u0.copy()
+    O.sweeps(O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, variant, fit.band_ranks, fit.store_rows),
+             level, src.data, ref, f, 3)
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, variant, fit.band_ranks, fit.store_rows, arow=src.data,
+                   simple=simple)
+    u = cuda(u0)
+    p.sweep(u, cuda(f), 3)
+    assert np.array_equal(u.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("simple", [True, False])
+def test_fast_mode_within_1e12(simple):
+    level, q = 6, 4
+    src, fit, u0 = _oracle_case(level, q)
+    f = np.zeros_like(u0)
+    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows)
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data, fast=True,
+                   simple=simple)
+    u, ref = cuda(u0), u0.copy()
+    for _ in range(5):
+        O.sweeps(sur, level, src.data, ref, f, 1)
+        p.sweep(u, cuda(f), 1)
+        assert relerr(u.cpu().numpy(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("simple", [True, False])
+def test_batched_tets_equal_single(simple):
+    """A batch [T, grid] sharing one surrogate equals T independent sweeps (config 4 path)."""
+    level, q = 5, 6
+    src, fit, u0 = _oracle_case(level, q, verts=lattice.kuhn_tet((0, 1, 2)))
+    T = 7
+    rng = np.random.default_rng(5)
+    us = np.stack([u0 * s for s in rng.uniform(0.5, 2.0, T)])
+    fs = np.zeros_like(us)
+    fs[2] = u0
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data,
+                   simple=simple)
+    ub = cuda(us)
+    rn = p.sweep(ub, cuda(fs), 2, norms=True)
+    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows)
+    for t in range(T):
+        ref = us[t].copy()
+        nr = O.sweeps(sur, level, src.data, ref, fs[t], 2, return_norms=True)
+        assert np.array_equal(ub[t].cpu().numpy(), ref)
+        np.testing.assert_allclose(rn[:, t].cpu().numpy(), nr, rtol=1e-12)
+
+
+def test_rate_three_digits_config1():
+    """configs[0]: L5 unit tet, q=4, 20 sweeps, f=0: last-step ratio equals the reference's
+    to 3 significant digits (bitwise in fact)."""
+    d = load("cfg1_L5_v1")
+    sm = SurrogateILUSmoother.setup(lattice.unit_tet(), 5, (4, 4, 4))
+    u = cuda(d["u0"])
+    norms = []
+    for _ in range(20):
+        sm.apply(u, cuda(d["f"]), 1)
+        norms.append(float(torch.linalg.norm(u)))
+    rho, rho_ref = norms[-1] / norms[-2], d["unorms"][-1] / d["unorms"][-2]
+    assert f"{rho:.3g}" == f"{rho_ref:.3g}"
+    assert np.array_equal(u.cpu().numpy(), d["u_after_20"])
+
+
+def test_solve_into_numpy_dropin():
+    d = load("cfg1_L5_v2")
+    sur = build_surrogate_ilu(S.stencil_source(lattice.unit_tet(), 5, S.CoefficientField.constant(1.0)), 5,
+                              (4, 4, 4), "v2")
+    w = d["solve_in"].copy()
+    sur.solve_into(w)
+    assert np.array_equal(w, d["solve_out"])
+
+
+def test_errors_fail_loudly():
+    d = load("cfg1_L5_v1")
+    p = plan_of(d, **op_of(d))
+    with pytest.raises(ValueError):
+        p.solve_into(torch.zeros(len(d["u0"]), dtype=torch.float64))          # CPU tensor
+    with pytest.raises(TypeError):
+        p.solve_into(torch.zeros(len(d["u0"]), dtype=torch.float32, device=DEV))
+    with pytest.raises(ValueError):
+        p.solve_into(torch.zeros(len(d["u0"]) + 1, dtype=torch.float64, device=DEV))
+    with pytest.raises(Exception):
+        DevicePlan(5, d["lcoefs"], d["dcoefs"], "v1", d["band_ranks"][:-1], d["store_rows"][:-1])

@@ -1,0 +1,93 @@
+"""P2: the product's host setup (stencil rows, native factorization, sampling, LSQ fit)
+reproduces the reference's arrays bitwise (golden vectors from the live reference)."""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from paper_2210_15280_b200 import fitting as F
+from paper_2210_15280_b200 import lattice
+from paper_2210_15280_b200 import stencil as S
+
+COEFF = {
+    "cfg1": lambda: S.CoefficientField.constant(1.0),
+    "cfg2": lambda: S.diag_tensor((1, 1, 1e-3)),
+    "cfg3": S.sin_kappa,
+    "cfg4": lambda: S.CoefficientField.constant(1.0),
+    "cfg5": lambda: S.diag_tensor((1, 1e-2, 1)),
+}
+CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "cfg*.npz")))
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name + ".npz"))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_stencil_rows_bitwise(name):
+    d = load(name)
+    src = S.stencil_source(d["verts"], int(d["level"]), COEFF[name[:4]]())
+    assert src.constant == bool(d["src_constant"])
+    assert np.array_equal(np.atleast_2d(src.data), d["arows"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_surrogate_fit_bitwise(name):
+    d = load(name)
+    L, q = int(d["level"]), int(d["q"])
+    src = S.stencil_source(d["verts"], L, COEFF[name[:4]]())
+    fit = F.fit_surrogate_ilu(src, L, (q, q, q), str(d["variant"]))
+    assert tuple(fit.degrees) == tuple(d["eff_degrees"])
+    assert fit.stride == int(d["stride"])
+    assert np.array_equal(fit.lcoefs, d["lcoefs"])
+    assert np.array_equal(fit.dcoefs, d["dcoefs"])
+    assert np.array_equal(fit.band_ranks, d["band_ranks"])
+    assert np.array_equal(fit.store_rows, d["store_rows"])
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if n in ("cfg1_L5_v1", "cfg2_L4_v1")])
+def test_native_factorization_bitwise(name):
+    d = load(name)
+    L = int(d["level"])
+    src = S.stencil_source(d["verts"], L, COEFF[name[:4]]())
+    assert np.array_equal(F.factorize_tet(src, L).rows, d["factors"])
+
+
+def test_operator_surrogate_fit_bitwise():
+    d = load("sop_L4")
+    src = S.stencil_source(lattice.unit_tet(), 4, S.sin_kappa())
+    assert np.array_equal(F.fit_surrogate_operator(src, 4, (3, 3, 3)), d["acoefs"])
+
+
+def test_pivot_breakdown_is_reported():
+    src = S.StencilSource(4, np.zeros(15), True)   # A = 0: the first pivot vanishes
+    with pytest.raises(F.PivotBreakdown) as ei:
+        F.factorize_tet(src, 4)
+    assert ei.value.coord == (1, 1, 1)
+
+
+def test_rank_deficient_fit_raises():
+    pts = np.zeros((10, 3))
+    with pytest.raises(F.RankDeficientFit):
+        F.lsq_fit(pts, np.ones(10), (1, 0, 0))
+    with pytest.raises(F.RankDeficientFit):
+        F.lsq_fit(np.ones((2, 3)), np.ones(2), (2, 2, 2))
+
+
+def test_lsq_exact_member_and_nddf():
+    rng = np.random.default_rng(0)
+    pts = rng.random((60, 3))
+    vals = 2 + 3 * pts[:, 0] * pts[:, 2]
+    poly = F.lsq_fit(pts, vals, (1, 0, 1))
+    np.testing.assert_allclose(poly.evaluate_scaled(pts), vals, atol=1e-12)
+    sq = F.SurrogatePolynomial((2, 0, 0), np.array([[[0.0]], [[0.0]], [[1.0]]]), 1.0)
+    np.testing.assert_array_equal(F.nddf_row_evaluate(sq, (0, 0, 0), 6), [0, 1, 4, 9, 16, 25])
+
+
+def test_unknown_variant():
+    src = S.stencil_source(lattice.unit_tet(), 3, S.CoefficientField.constant(1.0))
+    with pytest.raises(ValueError):
+        F.fit_surrogate_ilu(src, 3, (1, 1, 1), "v3")
