@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "tilu.h"
+#include "tilu_batch.cuh"
 #include "tilu_common.cuh"
 #include "tilu_plan.cuh"
 
@@ -26,6 +27,10 @@ bool launch_residual_sop(const PlanDev &P, const double *u, const double *f, dou
 void launch_reduce_rows(const double *part, int nrows, double *out, int ntets, cudaStream_t s);
 bool launch_simple_solve(const PlanDev &P, bool exact, bool stored, double *w, double *state, double *u, int ntets,
                          int which, cudaStream_t s);
+void launch_pack(const double *src, double *dst, int64_t grid, int ntets, cudaStream_t s);
+void launch_unpack(const double *src, double *dst, int64_t grid, int ntets, cudaStream_t s);
+void launch_batch_norms(const double *part, int nl, int ntets, double *out, cudaStream_t s);
+bool launch_batch_pass(const PlanDev &P, const BatchArgs &A, bool exact, bool fwd, cudaStream_t s);
 // plane-layout fast path (tilu_plane.cu)
 void prof_begin(cudaStream_t s);
 void prof_end(const char *name, cudaStream_t s);
@@ -129,6 +134,61 @@ struct Scratch {
 bool valid_plan(const tilu_plan_t *p) { return p != nullptr && p->dev.n > 0; }
 }  // namespace
 
+bool batch_ok(const tilu_plan_t *p)
+{
+    // packed element offsets are 32-bit: grid * 32 < 2^32 (level <= 9)
+    return !(p->flags & TILU_SCHED_SIMPLE) && p->dev.level <= 9 && p->dev.n >= 4 && p->bsched != nullptr;
+}
+
+size_t packed_doubles(const tilu_plan_t *p, int ntets) { return (size_t)((ntets + 31) / 32) * p->dev.grid * 32; }
+
+// `sweeps` fused sweeps on packed vectors (u, f, w all [G][grid][32]; w zero on the boundary).
+int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp, int ntets, int sweeps,
+                  double *rnorm2, cudaStream_t s)
+{
+    const PlanDev &P = p->dev;
+    const int G = (ntets + 31) / 32, nl = P.n - 3;
+    Scratch sc(s);
+    // sync block: [ticket_f, ticket_b, flags_f[G*nl], flags_b[G*nl]] as ints, reset to -1 per sweep
+    const size_t nsync = 2 + 2 * (size_t)G * nl;
+    int *sync = reinterpret_cast<int *>(sc.get((nsync + 1) / 2));
+    double *part = rnorm2 ? sc.get((size_t)G * nl * 32) : nullptr;
+    if (!sync || (rnorm2 && !part)) return fail(TILU_ENOMEM, "scratch allocation failed");
+    const bool exact = !(p->flags & TILU_FAST);
+    BatchArgs A{};
+    A.u = up;
+    A.f = fp;
+    A.w = wp;
+    A.G = G;
+    A.ntets = ntets;
+    A.sched = static_cast<const LayerSched *>(p->bsched);
+    A.Tmax = p->bTmax;
+    A.D = p->bD;
+    for (int k = 0; k < sweeps; ++k) {
+        cudaMemsetAsync(sync, 0xFF, nsync * sizeof(int), s);
+        A.ticket = sync;
+        A.flags = sync + 2;
+        A.part = part;
+        prof_begin(s);
+        bool ok = launch_batch_pass(P, A, exact, true, s);
+        prof_end("batch_fwd", s);
+        A.ticket = sync + 1;
+        A.flags = sync + 2 + (size_t)G * nl;
+        A.part = nullptr;
+        prof_begin(s);
+        ok = ok && launch_batch_pass(P, A, exact, false, s);
+        prof_end("batch_bwd", s);
+        if (!ok) return fail(TILU_EUNSUPPORTED, "kx+1 = %d not compiled", P.kx1);
+        g_launches += 2;
+        if (rnorm2) {
+            launch_batch_norms(part, nl, ntets, rnorm2 + (int64_t)k * ntets, s);
+            ++g_launches;
+        }
+    }
+    return TILU_OK;
+}
+
+
 extern "C" {
 
 void tilu_profile_enable(int on) { g_prof_on = on != 0; }
@@ -197,6 +257,15 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
     const int n = 1 << d->level;
     if (n < 4) return fail(TILU_EINVAL, "level too small");
 
+    {   // keep stream-ordered scratch cached between calls instead of returning it to the driver
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+    }
     tilu_plan *p = new (std::nothrow) tilu_plan();
     if (!p) return fail(TILU_ENOMEM, "host allocation failed");
     std::memset(p, 0, sizeof(*p));
@@ -302,6 +371,36 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
         }
         P.seedA = dseedA;
     }
+    {   // batched-path schedule (tilu_batch.cu header comment)
+        const int nl = n - 3;
+        std::vector<LayerSched> sch(nl);
+        int Bmax = 1;
+        for (int z = 1; z <= nl; ++z) {
+            const int R = n - 2 - z;
+            LayerSched &L = sch[z - 1];
+            L.A = std::max(2, (R + BW - 1) / BW);
+            L.B = L.A - 1;
+            Bmax = std::max(Bmax, L.B);
+        }
+        const int D = 2 * Bmax + 2;
+        int T = 0;
+        for (int z = 1; z <= nl; ++z) {
+            const int R = n - 2 - z;
+            LayerSched &L = sch[z - 1];
+            L.O = (z == 1) ? 0 : sch[z - 2].O + sch[z - 2].A * R - L.A * (R - 1) + 1 + D;
+            L.T0 = L.O;
+            L.T1 = L.O + std::max(L.A * (R - 1), n - 3 - z);
+            T = std::max(T, L.T1);
+        }
+        LayerSched *dsch = nullptr;
+        if ((rc = dev_upload(p, &dsch, sch.data(), sch.size()))) {
+            tilu_plan_destroy(p);
+            return rc;
+        }
+        p->bsched = dsch;
+        p->bTmax = T;
+        p->bD = D;
+    }
     launch_seed(P, dl, dd, dseedF, dseedB, 0);
     if (d->acoefs) launch_seed_op(P, dacoefs, d->aky1, d->akz1, dseedA, 0);
     if (cudaDeviceSynchronize() != cudaSuccess || (rc = check_cuda("seed tables"))) {
@@ -393,14 +492,26 @@ static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int nt
     if (stored && !p->dev.factors) return fail(TILU_EINVAL, "plan has no stored factors");
     if (sweeps == 0) return TILU_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!stored && !(p->flags & TILU_SCHED_SIMPLE) && plane_supported(p)) {
-        int launches = 0;
-        int rc = plane_sweep(p, u, f, ntets, sweeps, rnorm2, s, &launches);
-        g_launches = launches;
-        if (rc != TILU_OK) return fail(rc, "plane sweep failed: %s", cudaGetErrorString(cudaGetLastError()));
-        return check_cuda("plane sweep");
-    }
     const PlanDev &P = p->dev;
+    if (!stored && batch_ok(p) && ntets >= 2) {
+        // reference layout in, packed sweeps, reference layout out
+        Scratch sc(s);
+        const size_t pk = packed_doubles(p, ntets);
+        double *up = sc.get(pk), *fp = sc.get(pk), *wp = sc.get(pk);
+        if (!up || !fp || !wp) return fail(TILU_ENOMEM, "scratch allocation failed");
+        cudaMemsetAsync(wp, 0, pk * sizeof(double), s);
+        prof_begin(s);
+        launch_pack(u, up, P.grid, ntets, s);
+        launch_pack(f, fp, P.grid, ntets, s);
+        prof_end("pack", s);
+        int rc = packed_sweeps(p, up, fp, wp, ntets, sweeps, rnorm2, s);
+        if (rc) return rc;
+        prof_begin(s);
+        launch_unpack(up, u, P.grid, ntets, s);
+        prof_end("unpack", s);
+        g_launches += 3;
+        return check_cuda("batched sweep");
+    }
     Scratch sc(s);
     double *w = sc.get((size_t)ntets * P.grid);
     double *state = stored ? nullptr : sc.get((size_t)ntets * P.nrows * 8 * P.kx1);
@@ -421,6 +532,39 @@ static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int nt
         g_launches += 2;
     }
     return check_cuda("sweep");
+}
+
+int64_t tilu_packed_size(const tilu_plan_t *p, int ntets)
+{
+    return (p && ntets > 0) ? (int64_t)packed_doubles(p, ntets) : -1;
+}
+
+int tilu_pack(const tilu_plan_t *p, const double *src, double *dst, int ntets, void *stream)
+{
+    g_launches = 0;
+    if (!valid_plan(p) || !src || !dst || ntets < 1) return fail(TILU_EINVAL, "invalid arguments");
+    launch_pack(src, dst, p->dev.grid, ntets, static_cast<cudaStream_t>(stream));
+    g_launches = 1;
+    return check_cuda("pack");
+}
+
+int tilu_unpack(const tilu_plan_t *p, const double *src, double *dst, int ntets, void *stream)
+{
+    g_launches = 0;
+    if (!valid_plan(p) || !src || !dst || ntets < 1) return fail(TILU_EINVAL, "invalid arguments");
+    launch_unpack(src, dst, p->dev.grid, ntets, static_cast<cudaStream_t>(stream));
+    g_launches = 1;
+    return check_cuda("unpack");
+}
+
+int tilu_sweep_packed(const tilu_plan_t *p, double *u_p, const double *f_p, double *w_p, int ntets, int sweeps,
+                      double *rnorm2, void *stream)
+{
+    g_launches = 0;
+    if (!valid_plan(p) || !u_p || !f_p || !w_p || ntets < 1 || sweeps < 0) return fail(TILU_EINVAL, "invalid arguments");
+    if (!batch_ok(p)) return fail(TILU_EUNSUPPORTED, "packed sweeps need level <= 9 and the batched schedule");
+    int rc = packed_sweeps(p, u_p, f_p, w_p, ntets, sweeps, rnorm2, static_cast<cudaStream_t>(stream));
+    return rc ? rc : check_cuda("packed sweep");
 }
 
 int tilu_sweep(const tilu_plan_t *p, double *u, const double *f, int ntets, int sweeps, double *rnorm2, void *stream)

@@ -38,6 +38,9 @@ struct PlanDev {
 
 struct tilu_plan {
     tilu::PlanDev dev;
+    // batched (packed) path schedule
+    const void *bsched;  // device LayerSched[n-3]
+    int bTmax, bD;
     int flags;
     int64_t interior;
     int64_t nband;

@@ -112,6 +112,50 @@ class MacroMeshSmoother:
             torch.cuda.current_stream().wait_stream(self._side)
         return norms
 
+    # -- resident packed state (the hot path of the benchmark) ----------------------------------
+    def load(self, u: "torch.Tensor", f: "torch.Tensor") -> None:
+        """Move this rank's tets [ntets_local, grid] into the packed, interleaved device layout."""
+        self._res = []
+        for g, sm in zip(self.groups, self.smoothers):
+            idx = torch.as_tensor(g, device=u.device)
+            ug, fg = u.index_select(0, idx).contiguous(), f.index_select(0, idx).contiguous()
+            p = sm.plan
+            up, fp = p.pack(ug), p.pack(fg)
+            wp = torch.zeros_like(up)
+            self._res.append((sm, g, up, fp, wp))
+
+    def sweep(self, sweeps: int = 1, residual_norms: bool = True):
+        """``sweeps`` fused sweeps on the resident packed state; per-sweep global ||r||^2 is
+        allreduced on a side stream (overlapping the next sweep)."""
+        dev = self._res[0][2].device
+        norms = torch.zeros(sweeps, dtype=torch.float64, device=dev) if residual_norms else None
+        if residual_norms and self._side is None:
+            self._side = torch.cuda.Stream(device=dev)
+        for k in range(sweeps):
+            for sm, g, up, fp, wp in self._res:
+                rn = sm.plan.sweep_packed(up, fp, wp, len(g), 1, norms=residual_norms)
+                self.launches += sm.plan.last_launch_count()
+                if residual_norms:
+                    norms[k] += rn.sum()
+            if residual_norms:
+                ev = torch.cuda.Event()
+                ev.record()
+                with torch.cuda.stream(self._side):
+                    self._side.wait_event(ev)
+                    allreduce_norms(norms[k:k + 1], self.group)
+        if residual_norms:
+            torch.cuda.current_stream().wait_stream(self._side)
+        return norms
+
+    def store(self, u: "torch.Tensor") -> "torch.Tensor":
+        """Unpack the resident state back into u [ntets_local, grid] (reference layout)."""
+        for sm, g, up, fp, wp in self._res:
+            idx = torch.as_tensor(g, device=u.device)
+            ug = torch.empty((len(g), self.grid), dtype=u.dtype, device=u.device)
+            sm.plan.unpack(up, ug)
+            u.index_copy_(0, idx, ug)
+        return u
+
     def apply_host(self, u_host: "torch.Tensor", f_host: "torch.Tensor", sweeps: int = 1,
                    residual_norms: bool = True):
         """End-to-end call on (pinned) host tensors: H2D of u and f, ``sweeps`` sweeps, D2H of u
@@ -119,7 +163,9 @@ class MacroMeshSmoother:
         dev = torch.device("cuda", torch.cuda.current_device())
         u = u_host.to(dev, non_blocking=True)
         f = f_host.to(dev, non_blocking=True)
-        norms = self.apply(u, f, sweeps, residual_norms)
+        self.load(u, f)
+        norms = self.sweep(sweeps, residual_norms)
+        self.store(u)
         u_host.copy_(u, non_blocking=True)
         out = norms.to("cpu", non_blocking=True) if residual_norms else None
         torch.cuda.current_stream().synchronize()

@@ -152,6 +152,36 @@ class DevicePlan:
                       None if rn is None else rn.data_ptr(), _stream_ptr()))
         return rn
 
+    # -- packed (interleaved) batches: resident state for many tets sharing this plan ----------
+    def packed_numel(self, ntets: int) -> int:
+        return int(_lib.lib().tilu_packed_size(self._h, int(ntets)))
+
+    def pack(self, src, ntets: int | None = None, out=None):
+        src, T = _as_batch(src, self.grid, "src")
+        T = T if ntets is None else ntets
+        if out is None:
+            out = torch.empty(self.packed_numel(T), dtype=torch.float64, device=src.device)
+        _lib.check(_lib.lib().tilu_pack(self._h, src.data_ptr(), out.data_ptr(), T, _stream_ptr()))
+        return out
+
+    def unpack(self, src, out):
+        out, T = _as_batch(out, self.grid, "out")
+        if src.numel() != self.packed_numel(T):
+            raise ValueError("packed buffer size does not match ntets")
+        _lib.check(_lib.lib().tilu_unpack(self._h, src.data_ptr(), out.data_ptr(), T, _stream_ptr()))
+        return out
+
+    def sweep_packed(self, u_p, f_p, w_p, ntets: int, sweeps: int = 1, norms: bool = False):
+        """Fused sweeps on packed u, f (w_p: packed scratch, zero on the lattice boundary)."""
+        for name, t in (("u_p", u_p), ("f_p", f_p), ("w_p", w_p)):
+            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+                    and t.numel() == self.packed_numel(ntets)):
+                raise ValueError(f"{name}: packed CUDA fp64 buffer of {self.packed_numel(ntets)} doubles required")
+        rn = torch.empty((sweeps, ntets), dtype=torch.float64, device=u_p.device) if norms else None
+        _lib.check(_lib.lib().tilu_sweep_packed(self._h, u_p.data_ptr(), f_p.data_ptr(), w_p.data_ptr(), int(ntets),
+                                                int(sweeps), None if rn is None else rn.data_ptr(), _stream_ptr()))
+        return rn
+
     @staticmethod
     def last_launch_count() -> int:
         return _lib.last_launch_count()

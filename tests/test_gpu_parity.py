@@ -212,3 +212,94 @@ def test_errors_fail_loudly():
         p.solve_into(torch.zeros(len(d["u0"]) + 1, dtype=torch.float64, device=DEV))
     with pytest.raises(Exception):
         DevicePlan(5, d["lcoefs"], d["dcoefs"], "v1", d["band_ranks"][:-1], d["store_rows"][:-1])
+
+
+@pytest.mark.parametrize("T,level,q,variant", [(40, 5, 6, "v1"), (33, 4, 3, "v2"), (2, 6, 4, "v1")])
+def test_packed_batches_bitwise(T, level, q, variant):
+    """Interleaved fast path with padding groups (T not a multiple of 32), V1 and V2."""
+    src, fit, u0 = _oracle_case(level, q, variant, verts=lattice.kuhn_tet((2, 0, 1)))
+    rng = np.random.default_rng(T)
+    us = np.stack([u0 * s for s in rng.uniform(-2.0, 2.0, T)])
+    fs = np.zeros_like(us)
+    mask = lattice.interior_mask(level)
+    fs[:, mask] = rng.standard_normal((T, int(mask.sum())))
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, variant, fit.band_ranks, fit.store_rows, arow=src.data)
+    ub = cuda(us)
+    rn = p.sweep(ub, cuda(fs), 3, norms=True)
+    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, variant, fit.band_ranks, fit.store_rows)
+    for t in range(T):
+        ref = us[t].copy()
+        nr = O.sweeps(sur, level, src.data, ref, fs[t], 3, return_norms=True)
+        assert np.array_equal(ub[t].cpu().numpy(), ref), t
+        np.testing.assert_allclose(rn[:, t].cpu().numpy(), nr, rtol=1e-12)
+
+
+def test_packed_resident_api_and_roundtrip():
+    level, q, T = 5, 4, 37
+    src, fit, u0 = _oracle_case(level, q)
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data)
+    us = cuda(np.stack([u0 * (1 + 0.01 * t) for t in range(T)]))
+    back = torch.empty_like(us)
+    p.unpack(p.pack(us), back)
+    assert torch.equal(back, us)
+    up, fp = p.pack(us), p.pack(torch.zeros_like(us))
+    wp = torch.zeros_like(up)
+    p.sweep_packed(up, fp, wp, T, 2)
+    ref = us.clone()
+    p.sweep(ref, torch.zeros_like(us), 2)     # reference-layout entry point
+    p.unpack(up, back)
+    assert torch.equal(back, ref)
+
+
+def test_packed_fast_mode_within_1e12():
+    level, q, T = 6, 6, 5
+    src, fit, u0 = _oracle_case(level, q, verts=lattice.kuhn_tet((1, 2, 0)))
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data, fast=True)
+    us = np.stack([u0 * (t + 1) for t in range(T)])
+    ub = cuda(us)
+    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows)
+    refs = us.copy()
+    for _ in range(4):
+        p.sweep(ub, torch.zeros_like(ub), 1)
+        for t in range(T):
+            O.sweeps(sur, level, src.data, refs[t], np.zeros_like(u0), 1)
+        assert relerr(ub.cpu().numpy(), refs) <= 1e-12
+
+
+def test_config4_slice_level7_bitwise():
+    """Config 4 at full level: 33 Kuhn tets (one full group + padding group), L7, q=6 -> (4,4,5)."""
+    level, q, T = 7, 6, 33
+    src, fit, _ = _oracle_case(level, q, verts=lattice.kuhn_tet((0, 1, 2)))
+    assert tuple(fit.degrees) == (4, 4, 5)
+    mask = lattice.interior_mask(level)
+    rng = np.random.default_rng(4)
+    us = np.zeros((T, mask.size))
+    us[:, mask] = rng.uniform(-1, 1, (T, int(mask.sum())))
+    ub = cuda(us)
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data)
+    p.sweep(ub, torch.zeros_like(ub), 2)
+    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows)
+    got = ub.cpu().numpy()
+    for t in (0, 17, 31, 32):
+        ref = us[t].copy()
+        O.sweeps(sur, level, src.data, ref, np.zeros_like(ref), 2)
+        assert np.array_equal(got[t], ref), t
+
+
+def test_macro_mesh_smoother_resident_equals_apply():
+    from paper_2210_15280_b200 import MacroMeshSmoother
+    tets = lattice.kuhn_mesh(2)          # 48 tets
+    level = 4
+    mm = MacroMeshSmoother(tets, level, degrees=(3, 3, 3))
+    mask = lattice.interior_mask(level)
+    rng = np.random.default_rng(1)
+    us = np.zeros((len(tets), mask.size))
+    us[:, mask] = rng.uniform(-1, 1, (len(tets), int(mask.sum())))
+    u1, f = cuda(us), torch.zeros((len(tets), mask.size), dtype=torch.float64, device=DEV)
+    u2 = u1.clone()
+    n1 = mm.apply(u1, f, 3)
+    mm.load(u2, f)
+    n2 = mm.sweep(3)
+    mm.store(u2)
+    assert torch.equal(u1, u2)
+    torch.testing.assert_close(n1, n2, rtol=1e-12, atol=0)
