@@ -46,7 +46,7 @@ EXPORTS = (
     "tilu_stored_solve_into", "tilu_stored_sweep", "tilu_factorize_stream", "tilu_last_error",
     "tilu_version", "tilu_last_launch_count", "tilu_plan_grid_size", "tilu_plan_interior_size",
     "tilu_profile_enable", "tilu_profile_reset", "tilu_profile_read", "tilu_packed_size", "tilu_pack",
-    "tilu_unpack", "tilu_sweep_packed",
+    "tilu_unpack", "tilu_sweep_packed", "tilu_batch_schedule",
 )
 
 
@@ -89,6 +89,8 @@ def lib():
         getattr(L, name).restype = _I
     L.tilu_sweep_packed.argtypes = [_P, _P, _P, _P, _I, _I, _P, _P]
     L.tilu_sweep_packed.restype = _I
+    L.tilu_batch_schedule.argtypes = [_I, _P, _P, _P, _P, _P, _P]
+    L.tilu_batch_schedule.restype = _I
     L.tilu_profile_enable.argtypes = [_I]
     L.tilu_profile_enable.restype = None
     L.tilu_profile_reset.restype = None
@@ -124,3 +126,16 @@ def profile_read() -> dict:
         nm = names.raw[64 * i:64 * (i + 1)].split(b"\0", 1)[0].decode()
         out[nm] = (int(counts[i]), float(ms[i]))
     return out
+
+
+def batch_schedule(level: int) -> dict:
+    """The batched path's per-layer schedule as computed by libtilu (host only)."""
+    import numpy as np
+    nl = 2 ** level - 3
+    A, B, O, T1 = (np.zeros(max(nl, 1), dtype=np.int32) for _ in range(4))
+    D, Tmax = ctypes.c_int(), ctypes.c_int()
+    k = lib().tilu_batch_schedule(level, A.ctypes.data, B.ctypes.data, O.ctypes.data, T1.ctypes.data,
+                                  ctypes.byref(D), ctypes.byref(Tmax))
+    if k < 0:
+        check(-k)
+    return {"A": A[:k], "B": B[:k], "O": O[:k], "T1": T1[:k], "D": D.value, "Tmax": Tmax.value}

@@ -134,6 +134,32 @@ struct Scratch {
 bool valid_plan(const tilu_plan_t *p) { return p != nullptr && p->dev.n > 0; }
 }  // namespace
 
+// Batched-path schedule (tilu_batch.cu header comment): per layer z the row skew A_z, window
+// B_z = A_z - 1, first-point step O_z and last step T1_z; D = cross-layer slack.
+void batch_schedule(int n, std::vector<LayerSched> &sch, int &Tmax, int &D)
+{
+    const int nl = n - 3;
+    sch.assign(nl, LayerSched{});
+    int Bmax = 1;
+    for (int z = 1; z <= nl; ++z) {
+        const int R = n - 2 - z;
+        LayerSched &L = sch[z - 1];
+        L.A = std::max(2, (R + BW - 1) / BW);
+        L.B = L.A - 1;
+        Bmax = std::max(Bmax, L.B);
+    }
+    D = 2 * Bmax + 2;
+    Tmax = 0;
+    for (int z = 1; z <= nl; ++z) {
+        const int R = n - 2 - z;
+        LayerSched &L = sch[z - 1];
+        L.O = (z == 1) ? 0 : sch[z - 2].O + sch[z - 2].A * R - L.A * (R - 1) + 1 + D;
+        L.T0 = L.O;
+        L.T1 = L.O + std::max(L.A * (R - 1), n - 3 - z);
+        Tmax = std::max(Tmax, L.T1);
+    }
+}
+
 bool batch_ok(const tilu_plan_t *p)
 {
     // packed element offsets are 32-bit: grid * 32 < 2^32 (level <= 9)
@@ -371,27 +397,10 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
         }
         P.seedA = dseedA;
     }
-    {   // batched-path schedule (tilu_batch.cu header comment)
-        const int nl = n - 3;
-        std::vector<LayerSched> sch(nl);
-        int Bmax = 1;
-        for (int z = 1; z <= nl; ++z) {
-            const int R = n - 2 - z;
-            LayerSched &L = sch[z - 1];
-            L.A = std::max(2, (R + BW - 1) / BW);
-            L.B = L.A - 1;
-            Bmax = std::max(Bmax, L.B);
-        }
-        const int D = 2 * Bmax + 2;
-        int T = 0;
-        for (int z = 1; z <= nl; ++z) {
-            const int R = n - 2 - z;
-            LayerSched &L = sch[z - 1];
-            L.O = (z == 1) ? 0 : sch[z - 2].O + sch[z - 2].A * R - L.A * (R - 1) + 1 + D;
-            L.T0 = L.O;
-            L.T1 = L.O + std::max(L.A * (R - 1), n - 3 - z);
-            T = std::max(T, L.T1);
-        }
+    {
+        std::vector<LayerSched> sch;
+        int T = 0, D = 0;
+        batch_schedule(n, sch, T, D);
         LayerSched *dsch = nullptr;
         if ((rc = dev_upload(p, &dsch, sch.data(), sch.size()))) {
             tilu_plan_destroy(p);
@@ -532,6 +541,20 @@ static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int nt
         g_launches += 2;
     }
     return check_cuda("sweep");
+}
+
+int tilu_batch_schedule(int level, int *A, int *B, int *O, int *T1, int *D, int *Tmax)
+{
+    if (level < 2 || level > 10) return fail(TILU_EINVAL, "level %d outside 2..10", level);
+    std::vector<LayerSched> sch;
+    batch_schedule(1 << level, sch, *Tmax, *D);
+    for (size_t i = 0; i < sch.size(); ++i) {
+        A[i] = sch[i].A;
+        B[i] = sch[i].B;
+        O[i] = sch[i].O;
+        T1[i] = sch[i].T1;
+    }
+    return (int)sch.size();
 }
 
 int64_t tilu_packed_size(const tilu_plan_t *p, int ntets)

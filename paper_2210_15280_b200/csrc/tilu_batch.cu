@@ -41,6 +41,17 @@ __device__ __forceinline__ void st_release(int *p, int v)
 }
 __device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
 
+// Thread 0 waits until the neighbouring layer's progress counter reaches `need`.  A schedule bug
+// must fail loudly, not hang the device: after ~10 s of polling the kernel traps.
+__device__ __forceinline__ void wait_progress(const int *flag, int need)
+{
+    long long polls = 0;
+    while (ld_acquire(flag) < need) {
+        __nanosleep(64);
+        if (++polls > (1ll << 27)) __trap();
+    }
+}
+
 __device__ __forceinline__ bool in_band_b(int x, int y, int z, int xe) { return z == 1 || y == 1 || x == 1 || x == xe; }
 __device__ __forceinline__ int band_idx_b(const PlanDev &P, int row, int x, int y, int z)
 {
@@ -96,8 +107,10 @@ __global__ void __launch_bounds__(BW * 32, 2) k_batch_fwd(PlanDev P, BatchArgs A
 
     for (int tau0 = S.T0; tau0 <= S.T1; tau0 += S.B) {
         if (threadIdx.x == 0 && below) {
-            const int need = tau0 + S.B - 2 - A.D;
-            while (ld_acquire(below) < need) __nanosleep(40);
+            // everything this window reads from layer z-1 has T <= tau0 + B - 2 - D; the layer below
+            // never publishes beyond its own last step
+            const int need = min(tau0 + S.B - 2 - A.D, A.sched[zi - 1].T1);
+            wait_progress(below, need);
         }
         __syncthreads();
         const int tau1 = min(tau0 + S.B, S.T1 + 1);
@@ -257,8 +270,8 @@ __global__ void __launch_bounds__(BW * 32, 2) k_batch_bwd(PlanDev P, BatchArgs A
 
     for (int tau0 = tb0; tau0 <= tb1; tau0 += S.B) {
         if (threadIdx.x == 0 && above) {
-            const int need = tau0 + S.B - 2 - A.D;
-            while (ld_acquire(above) < need) __nanosleep(40);
+            const int need = min(tau0 + S.B - 2 - A.D, A.Tmax - A.sched[zi + 1].T0);
+            wait_progress(above, need);
         }
         __syncthreads();
         const int tau1 = min(tau0 + S.B, tb1 + 1);
