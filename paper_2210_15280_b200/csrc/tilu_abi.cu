@@ -134,32 +134,6 @@ struct Scratch {
 bool valid_plan(const tilu_plan_t *p) { return p != nullptr && p->dev.n > 0; }
 }  // namespace
 
-// Batched-path schedule (tilu_batch.cu header comment): per layer z the row skew A_z, window
-// B_z = A_z - 1, first-point step O_z and last step T1_z; D = cross-layer slack.
-void batch_schedule(int n, std::vector<LayerSched> &sch, int &Tmax, int &D)
-{
-    const int nl = n - 3;
-    sch.assign(nl, LayerSched{});
-    int Bmax = 1;
-    for (int z = 1; z <= nl; ++z) {
-        const int R = n - 2 - z;
-        LayerSched &L = sch[z - 1];
-        L.A = std::max(2, (R + BW - 1) / BW);
-        L.B = L.A - 1;
-        Bmax = std::max(Bmax, L.B);
-    }
-    D = 2 * Bmax + 2;
-    Tmax = 0;
-    for (int z = 1; z <= nl; ++z) {
-        const int R = n - 2 - z;
-        LayerSched &L = sch[z - 1];
-        L.O = (z == 1) ? 0 : sch[z - 2].O + sch[z - 2].A * R - L.A * (R - 1) + 1 + D;
-        L.T0 = L.O;
-        L.T1 = L.O + std::max(L.A * (R - 1), n - 3 - z);
-        Tmax = std::max(Tmax, L.T1);
-    }
-}
-
 bool batch_ok(const tilu_plan_t *p)
 {
     // packed element offsets are 32-bit: grid * 32 < 2^32 (level <= 9)
@@ -188,6 +162,7 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
     A.G = G;
     A.ntets = ntets;
     A.sched = static_cast<const LayerSched *>(p->bsched);
+    A.rows = static_cast<const RowSched *>(p->brows);
     A.Tmax = p->bTmax;
     A.D = p->bD;
     for (int k = 0; k < sweeps; ++k) {
@@ -399,14 +374,17 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
     }
     {
         std::vector<LayerSched> sch;
+        std::vector<RowSched> rsch;
         int T = 0, D = 0;
-        batch_schedule(n, sch, T, D);
+        batch_schedule(n, sch, rsch, T, D);
         LayerSched *dsch = nullptr;
-        if ((rc = dev_upload(p, &dsch, sch.data(), sch.size()))) {
+        RowSched *drs = nullptr;
+        if ((rc = dev_upload(p, &dsch, sch.data(), sch.size())) || (rc = dev_upload(p, &drs, rsch.data(), rsch.size()))) {
             tilu_plan_destroy(p);
             return rc;
         }
         p->bsched = dsch;
+        p->brows = drs;
         p->bTmax = T;
         p->bD = D;
     }
@@ -543,18 +521,22 @@ static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int nt
     return check_cuda("sweep");
 }
 
-int tilu_batch_schedule(int level, int *A, int *B, int *O, int *T1, int *D, int *Tmax)
+int tilu_batch_schedule(int level, int *row_start, int *row_warp, int *layer_T1, int *D, int *Tmax)
 {
-    if (level < 2 || level > 10) return fail(TILU_EINVAL, "level %d outside 2..10", level);
+    if (level < 2 || level > 10) return -fail(TILU_EINVAL, "level %d outside 2..10", level);
+    const int n = 1 << level;
     std::vector<LayerSched> sch;
-    batch_schedule(1 << level, sch, *Tmax, *D);
-    for (size_t i = 0; i < sch.size(); ++i) {
-        A[i] = sch[i].A;
-        B[i] = sch[i].B;
-        O[i] = sch[i].O;
-        T1[i] = sch[i].T1;
+    std::vector<RowSched> rs;
+    batch_schedule(n, sch, rs, *Tmax, *D);
+    for (int z = 1; z <= n - 3; ++z) {
+        layer_T1[z - 1] = sch[z - 1].T1;
+        for (int wi = 0; wi < BW; ++wi)
+            for (int y = sch[z - 1].first[wi]; y; y = rs[row_id(n, z, y)].next) {
+                row_start[row_id(n, z, y)] = rs[row_id(n, z, y)].start;
+                row_warp[row_id(n, z, y)] = wi;
+            }
     }
-    return (int)sch.size();
+    return (n - 3) * (n - 2) / 2;
 }
 
 int64_t tilu_packed_size(const tilu_plan_t *p, int ntets)

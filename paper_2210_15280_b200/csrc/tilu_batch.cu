@@ -7,22 +7,28 @@
 // coalesced 256 B access, no lane is ever idle, and each lane executes exactly the reference's
 // serial operation sequence for its own tet (bitwise parity in exact mode).
 //
-// Schedule: one CTA per (group, z-layer), BW warps per CTA, row y of layer z handled by warp
-// (y-1) % BW.  Point (x, y, z) runs at global step T = O_z + A_z (y-1) + (x-1):
-//   * A_z >= 2 row skew inside a layer, A_z * BW >= longest row so a warp owns one row at a
-//     time; row y needs row y-1's values from >= A_z - 1 steps earlier, so the CTA
-//     synchronises only every B_z = A_z - 1 steps (one bar.sync per window, not per step);
-//   * O_z - O_{z-1} = A_{z-1} R_z - A_z (R_z - 1) + 1 + D: every value a layer needs from the
-//     layer below was produced >= D + 1 steps earlier.  Layers run in different CTAs (often on
-//     different SMs) and hand over through release/acquire progress counters; D is slack so the
-//     consumer rarely waits.
+// Schedule: one CTA per (group, z-layer), BW warps per CTA, each warp owns one row of the layer
+// at a time.  A host-side greedy list schedule (batch_schedule below) gives every row (y, z) a
+// start step S: point (x, y, z) runs at forward step S + x - 1, rows start in y order as soon as
+//   * a warp of the CTA is free,
+//   * S(y) >= S(y-1) + AMIN: row y reads row y-1 (same layer, another warp) only from
+//     synchronisation windows already closed by a CTA barrier, even one point ahead (prefetch);
+//     the CTA therefore synchronises once per BWIN steps, not per step;
+//   * S_z(y) >= S_{z-1}(y+1) + 1 + D and >= S_{z-1}(y) + 2 + D: everything read from the layer
+//     below (another CTA, usually another SM) was produced >= D + 1 steps earlier.  Layers hand
+//     over through release/acquire progress counters published at every window end; D is slack
+//     so the consumer rarely waits.
 // The backward pass runs the exact time reversal of this schedule (T_b = Tmax - T), which
 // satisfies the transposed dependencies.  CTAs take (group, layer) tickets in layer order
 // (ascending z forward, descending backward), so a CTA only ever waits for CTAs that already
-// hold earlier tickets: no deadlock whatever the residency.
+// hold earlier tickets: no deadlock whatever the residency.  tests/test_schedule.py verifies
+// dependencies, warp exclusivity and handoff completion on the host.
 //
 // Forward kernel  = residual f - A u (15-point stencil) + forward L substitution, writes w.
 // Backward kernel = D^{-1} scaling + L^T substitution + u += w, writes w (in place) and u.
+// Every load of point x+1 is issued while point x computes (one-point software prefetch).
+#include <algorithm>
+
 #include "tilu_batch.cuh"
 #include "tilu_common.cuh"
 #include "tilu_plan.cuh"
@@ -70,10 +76,60 @@ __device__ __forceinline__ double lq_b(const PlanDev &P, int m, int qx, int qy, 
 }
 
 // ----------------------------------------------------------------------------------------------
+// host: greedy list schedule
+// ----------------------------------------------------------------------------------------------
+void batch_schedule(int n, std::vector<LayerSched> &layers, std::vector<RowSched> &rows, int &Tmax, int &D)
+{
+    const int nl = n - 3;
+    D = 2 * BWIN + 2;
+    layers.assign(nl, LayerSched{});
+    rows.assign((size_t)(n - 3) * (n - 2) / 2 + 1, RowSched{0, 0, 0});
+    Tmax = 0;
+    for (int z = 1; z <= nl; ++z) {
+        const int R = n - 2 - z;
+        LayerSched &L = layers[z - 1];
+        int free_at[BW], lastrow[BW];
+        for (int w = 0; w < BW; ++w) {
+            free_at[w] = 0;
+            lastrow[w] = 0;
+            L.first[w] = L.last[w] = 0;
+        }
+        int prev_start = -(1 << 29);
+        L.T0 = 1 << 30;
+        L.T1 = 0;
+        for (int y = 1; y <= R; ++y) {
+            const int m = n - 1 - z - y;
+            int t = std::max(0, prev_start + AMIN);
+            if (z > 1) {
+                t = std::max(t, rows[row_id(n, z - 1, y + 1)].start + 1 + D);
+                t = std::max(t, rows[row_id(n, z - 1, y)].start + 2 + D);
+            }
+            int wbest = 0;
+            for (int w = 1; w < BW; ++w)
+                if (free_at[w] < free_at[wbest]) wbest = w;
+            t = std::max(t, free_at[wbest]);
+            RowSched &rs = rows[row_id(n, z, y)];
+            rs.start = t;
+            rs.next = 0;
+            rs.prev = lastrow[wbest];
+            if (lastrow[wbest]) rows[row_id(n, z, lastrow[wbest])].next = y;
+            else L.first[wbest] = y;
+            lastrow[wbest] = y;
+            L.last[wbest] = y;
+            free_at[wbest] = t + m;
+            prev_start = t;
+            L.T0 = std::min(L.T0, t);
+            L.T1 = std::max(L.T1, t + m - 1);
+        }
+        Tmax = std::max(Tmax, L.T1);
+    }
+}
+
+// ----------------------------------------------------------------------------------------------
 // forward: residual + L solve
 // ----------------------------------------------------------------------------------------------
 template <int K, bool EXACT, bool CONST_ROW>
-__global__ void __launch_bounds__(BW * 32, 2) k_batch_fwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(BW * 32, 1) k_batch_fwd(PlanDev P, BatchArgs A)
 {
     __shared__ int s_ticket;
     __shared__ double s_red[BW][32];
@@ -82,14 +138,15 @@ __global__ void __launch_bounds__(BW * 32, 2) k_batch_fwd(PlanDev P, BatchArgs A
     __syncthreads();
     const int nl = P.n - 3;
     const int zi = s_ticket / A.G, g = s_ticket - (s_ticket / A.G) * A.G;
-    const int n = P.n, z = zi + 1, R = n - 2 - z;
-    const LayerSched S = A.sched[zi];
+    const int n = P.n, z = zi + 1;
+    const int T0 = A.sched[zi].T0, T1 = A.sched[zi].T1;
     const size_t gb = (size_t)g * P.grid * 32 + lane;
     const double *__restrict__ u = A.u + gb;
     const double *__restrict__ f = A.f + gb;
     double *__restrict__ w = A.w + gb;
     int *myflag = A.flags + g * nl + zi;
     const int *below = z > 1 ? myflag - 1 : nullptr;
+    const int belowT1 = z > 1 ? A.sched[zi - 1].T1 : 0;
 
     double a[15];
     if (CONST_ROW) {
@@ -97,28 +154,28 @@ __global__ void __launch_bounds__(BW * 32, 2) k_batch_fwd(PlanDev P, BatchArgs A
         for (int i = 0; i < 15; ++i) a[i] = P.arow[i];
     }
 
-    int y = warp + 1;
-    int m = 0, rid = 0;
+    int y = A.sched[zi].first[warp];
+    int m = 0, rid = 0, start = 0;
     uint32_t oc = 0, os = 0, on = 0, obn = 0, obc = 0, ots = 0, otc = 0;
     double d[7][K];
+    // sliding windows: values of point x-1 / x that point x+1 reuses
     double u_wm = 0, u_c = 0, us0 = 0, un_m = 0, ubn_m = 0, ubc0 = 0, uts0 = 0, utc_m = 0;
     double ws0 = 0, wbn_m = 0, wbc0 = 0, wprev = 0;
+    // newest entries of the current point (prefetched while the previous point computed)
+    double c_ue = 0, c_us = 0, c_un = 0, c_ubn = 0, c_ubc = 0, c_uts = 0, c_utc = 0, c_f = 0;
+    double c_ws = 0, c_wbn = 0, c_wbc = 0;
     double ss = 0.0;
+    if (y) start = A.rows[row_id(n, z, y)].start;
 
-    for (int tau0 = S.T0; tau0 <= S.T1; tau0 += S.B) {
-        if (threadIdx.x == 0 && below) {
-            // everything this window reads from layer z-1 has T <= tau0 + B - 2 - D; the layer below
-            // never publishes beyond its own last step
-            const int need = min(tau0 + S.B - 2 - A.D, A.sched[zi - 1].T1);
-            wait_progress(below, need);
-        }
+    for (int tau0 = T0; tau0 <= T1; tau0 += BWIN) {
+        if (threadIdx.x == 0 && below) wait_progress(below, min(tau0 + BWIN - 1 - A.D, belowT1));
         __syncthreads();
-        const int tau1 = min(tau0 + S.B, S.T1 + 1);
+        const int tau1 = min(tau0 + BWIN, T1 + 1);
         for (int tau = tau0; tau < tau1; ++tau) {
-            if (y > R) break;
-            const int x = tau - (S.O + S.A * (y - 1)) + 1;
+            if (!y) break;
+            const int x = tau - start + 1;
             if (x < 1) continue;
-            if (x == 1) {  // row start: offsets, seed table, stencil windows
+            if (x == 1) {  // row start: offsets, seed table, stencil windows, point-1 values
                 m = n - 1 - z - y;
                 rid = row_id(n, z, y);
                 oc = (uint32_t)row_offset(n, z, y) * 32u;
@@ -145,13 +202,36 @@ __global__ void __launch_bounds__(BW * 32, 2) k_batch_fwd(PlanDev P, BatchArgs A
                 wbn_m = ldcg(w + obn);
                 wbc0 = ldcg(w + obc + 32);
                 wprev = 0.0;
+                c_ue = u[oc + 64];
+                c_us = u[os + 64];
+                c_un = u[on + 32];
+                c_ubn = u[obn + 32];
+                c_ubc = u[obc + 64];
+                c_uts = u[ots + 64];
+                c_utc = u[otc + 32];
+                c_f = f[oc + 32];
+                c_ws = ldcg(w + os + 64);
+                c_wbn = ldcg(w + obn + 32);
+                c_wbc = ldcg(w + obc + 64);
             }
             const uint32_t X = (uint32_t)x * 32u;
-            // newest window entries
-            const double u_e = u[oc + X + 32], us1 = u[os + X + 32], un0 = u[on + X];
-            const double ubn0 = u[obn + X], ubc1 = u[obc + X + 32], uts1 = u[ots + X + 32], utc0 = u[otc + X];
-            const double fx = f[oc + X];
-            const double ws1 = ldcg(w + os + X + 32), wbn0 = ldcg(w + obn + X), wbc1 = ldcg(w + obc + X + 32);
+            // prefetch point x+1 (safe: AMIN and the window's progress wait cover it)
+            double n_ue = 0, n_us = 0, n_un = 0, n_ubn = 0, n_ubc = 0, n_uts = 0, n_utc = 0, n_f = 0;
+            double n_ws = 0, n_wbn = 0, n_wbc = 0;
+            if (x < m) {
+                const uint32_t X1 = X + 32u;
+                n_ue = u[oc + X1 + 32];
+                n_us = u[os + X1 + 32];
+                n_un = u[on + X1];
+                n_ubn = u[obn + X1];
+                n_ubc = u[obc + X1 + 32];
+                n_uts = u[ots + X1 + 32];
+                n_utc = u[otc + X1];
+                n_f = f[oc + X1];
+                n_ws = ldcg(w + os + X1 + 32);
+                n_wbn = ldcg(w + obn + X1);
+                n_wbc = ldcg(w + obc + X1 + 32);
+            }
             if (!CONST_ROW) {
                 const double *ar = P.arows + 15 * (int64_t)(oc / 32u + x);
 #pragma unroll
@@ -161,19 +241,19 @@ __global__ void __launch_bounds__(BW * 32, 2) k_batch_fwd(PlanDev P, BatchArgs A
             double acc = EXACT ? dmul(a[7], u_c) : a[7] * u_c;
             acc = madd<EXACT>(acc, a[0], u_wm);
             acc = madd<EXACT>(acc, a[1], us0);
-            acc = madd<EXACT>(acc, a[2], us1);
+            acc = madd<EXACT>(acc, a[2], c_us);
             acc = madd<EXACT>(acc, a[3], ubn_m);
-            acc = madd<EXACT>(acc, a[4], ubn0);
+            acc = madd<EXACT>(acc, a[4], c_ubn);
             acc = madd<EXACT>(acc, a[5], ubc0);
-            acc = madd<EXACT>(acc, a[6], ubc1);
-            acc = madd<EXACT>(acc, a[8], u_e);
-            acc = madd<EXACT>(acc, a[9], un0);
+            acc = madd<EXACT>(acc, a[6], c_ubc);
+            acc = madd<EXACT>(acc, a[8], c_ue);
+            acc = madd<EXACT>(acc, a[9], c_un);
             acc = madd<EXACT>(acc, a[10], un_m);
-            acc = madd<EXACT>(acc, a[11], uts1);
+            acc = madd<EXACT>(acc, a[11], c_uts);
             acc = madd<EXACT>(acc, a[12], uts0);
-            acc = madd<EXACT>(acc, a[13], utc0);
+            acc = madd<EXACT>(acc, a[13], c_utc);
             acc = madd<EXACT>(acc, a[14], utc_m);
-            const double r = dsub(fx, acc);
+            const double r = dsub(c_f, acc);
             ss = fma(r, r, ss);
             // L entries: NDDF marchers or the V1 band store
             double L[7];
@@ -189,18 +269,18 @@ __global__ void __launch_bounds__(BW * 32, 2) k_batch_fwd(PlanDev P, BatchArgs A
             if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
                 v = msub<true>(r, L[0], wprev);
                 v = msub<true>(v, L[1], ws0);
-                v = msub<true>(v, L[2], ws1);
+                v = msub<true>(v, L[2], c_ws);
                 v = msub<true>(v, L[3], wbn_m);
-                v = msub<true>(v, L[4], wbn0);
+                v = msub<true>(v, L[4], c_wbn);
                 v = msub<true>(v, L[5], wbc0);
-                v = msub<true>(v, L[6], wbc1);
+                v = msub<true>(v, L[6], c_wbc);
             } else {      // own-row term last: one FMA on the row's dependency chain
                 v = msub<false>(r, L[1], ws0);
-                v = msub<false>(v, L[2], ws1);
+                v = msub<false>(v, L[2], c_ws);
                 v = msub<false>(v, L[3], wbn_m);
-                v = msub<false>(v, L[4], wbn0);
+                v = msub<false>(v, L[4], c_wbn);
                 v = msub<false>(v, L[5], wbc0);
-                v = msub<false>(v, L[6], wbc1);
+                v = msub<false>(v, L[6], c_wbc);
                 v = msub<false>(v, L[0], wprev);
             }
             w[oc + X] = v;
@@ -208,18 +288,32 @@ __global__ void __launch_bounds__(BW * 32, 2) k_batch_fwd(PlanDev P, BatchArgs A
             for (int mm = 0; mm < 7; ++mm) march<K>(d[mm]);
             // slide the windows
             u_wm = u_c;
-            u_c = u_e;
-            us0 = us1;
-            un_m = un0;
-            ubn_m = ubn0;
-            ubc0 = ubc1;
-            uts0 = uts1;
-            utc_m = utc0;
-            ws0 = ws1;
-            wbn_m = wbn0;
-            wbc0 = wbc1;
+            u_c = c_ue;
+            us0 = c_us;
+            un_m = c_un;
+            ubn_m = c_ubn;
+            ubc0 = c_ubc;
+            uts0 = c_uts;
+            utc_m = c_utc;
+            ws0 = c_ws;
+            wbn_m = c_wbn;
+            wbc0 = c_wbc;
             wprev = v;
-            if (x == m) y += BW;
+            c_ue = n_ue;
+            c_us = n_us;
+            c_un = n_un;
+            c_ubn = n_ubn;
+            c_ubc = n_ubc;
+            c_uts = n_uts;
+            c_utc = n_utc;
+            c_f = n_f;
+            c_ws = n_ws;
+            c_wbn = n_wbn;
+            c_wbc = n_wbc;
+            if (x == m) {
+                y = A.rows[rid].next;
+                if (y) start = A.rows[row_id(n, z, y)].start;
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -243,45 +337,42 @@ __global__ void __launch_bounds__(BW * 32, 2) k_batch_fwd(PlanDev P, BatchArgs A
 // backward: D^{-1} + L^T solve + update, exact time reversal of the forward schedule
 // ----------------------------------------------------------------------------------------------
 template <int K, bool EXACT>
-__global__ void __launch_bounds__(BW * 32, 2) k_batch_bwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(BW * 32, 1) k_batch_bwd(PlanDev P, BatchArgs A)
 {
     __shared__ int s_ticket;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(A.ticket, 1) + 1;  // counter starts at -1
+    if (threadIdx.x == 0) s_ticket = atomicAdd(A.ticket, 1) + 1;
     __syncthreads();
     const int nl = P.n - 3;
     const int li = s_ticket / A.G, g = s_ticket - li * A.G;
     const int zi = nl - 1 - li;
-    const int n = P.n, z = zi + 1, R = n - 2 - z;
-    const LayerSched S = A.sched[zi];
+    const int n = P.n, z = zi + 1;
     const size_t gb = (size_t)g * P.grid * 32 + lane;
     double *__restrict__ u = A.u + gb;
     double *__restrict__ w = A.w + gb;
     int *myflag = A.flags + g * nl + zi;
     const int *above = z < nl ? myflag + 1 : nullptr;
+    const int aboveEnd = z < nl ? A.Tmax - A.sched[zi + 1].T0 : 0;
+    const int tb0 = A.Tmax - A.sched[zi].T1, tb1 = A.Tmax - A.sched[zi].T0;
 
-    // the warp's rows in descending order
-    int y = warp < R ? warp + 1 + ((R - 1 - warp) / BW) * BW : 0;  // largest y <= R with (y-1) % BW == warp
-    int m = 0, rid = 0;
+    int y = A.sched[zi].last[warp];
+    int m = 0, rid = 0, bstart = 0;  // bstart: backward step of the row's first point (x = m)
     uint32_t oc = 0, on = 0, ots = 0, otc = 0;
     double d[8][K];
     double wn_hi = 0, wts_hi = 0, wtc_hi = 0, wprev = 0;
-    const int tb0 = A.Tmax - S.T1, tb1 = A.Tmax - S.T0;
+    double c_wn = 0, c_wts = 0, c_wtc = 0, c_wf = 0, c_u = 0;
+    if (y) bstart = A.Tmax - (A.rows[row_id(n, z, y)].start + (n - 1 - z - y) - 1);
 
-    for (int tau0 = tb0; tau0 <= tb1; tau0 += S.B) {
-        if (threadIdx.x == 0 && above) {
-            const int need = min(tau0 + S.B - 2 - A.D, A.Tmax - A.sched[zi + 1].T0);
-            wait_progress(above, need);
-        }
+    for (int tau0 = tb0; tau0 <= tb1; tau0 += BWIN) {
+        if (threadIdx.x == 0 && above) wait_progress(above, min(tau0 + BWIN - 1 - A.D, aboveEnd));
         __syncthreads();
-        const int tau1 = min(tau0 + S.B, tb1 + 1);
+        const int tau1 = min(tau0 + BWIN, tb1 + 1);
         for (int tau = tau0; tau < tau1; ++tau) {
-            if (y < 1) break;
-            const int mrow = n - 1 - z - y;
-            const int x = A.Tmax - tau - (S.O + S.A * (y - 1)) + 1;
-            if (x > mrow) continue;
-            if (x == mrow) {  // row start (x descending)
-                m = mrow;
+            if (!y) break;
+            const int k = tau - bstart;  // 0-based position along the descending row
+            if (k < 0) continue;
+            if (k == 0) {  // row start at x = m
+                m = n - 1 - z - y;
                 rid = row_id(n, z, y);
                 oc = (uint32_t)row_offset(n, z, y) * 32u;
                 on = (uint32_t)row_offset(n, z, y + 1) * 32u;
@@ -297,11 +388,23 @@ __global__ void __launch_bounds__(BW * 32, 2) k_batch_bwd(PlanDev P, BatchArgs A
                 wts_hi = ldcg(w + ots + M + 32);
                 wtc_hi = ldcg(w + otc + M);
                 wprev = 0.0;
+                c_wn = ldcg(w + on + M - 32);
+                c_wts = ldcg(w + ots + M);
+                c_wtc = ldcg(w + otc + M - 32);
+                c_wf = w[oc + M];
+                c_u = u[oc + M];
             }
+            const int x = m - k;
             const uint32_t X = (uint32_t)x * 32u;
-            const double wn_lo = ldcg(w + on + X - 32), wts_lo = ldcg(w + ots + X), wtc_lo = ldcg(w + otc + X - 32);
-            const double wf = w[oc + X];
-            const double uo = u[oc + X];
+            double n_wn = 0, n_wts = 0, n_wtc = 0, n_wf = 0, n_u = 0;
+            if (x > 1) {
+                const uint32_t X1 = X - 32u;
+                n_wn = ldcg(w + on + X1 - 32);
+                n_wts = ldcg(w + ots + X1);
+                n_wtc = ldcg(w + otc + X1 - 32);
+                n_wf = w[oc + X1];
+                n_u = u[oc + X1];
+            }
             const bool band = P.variant == 1 && in_band_b(x, y, z, m);
             const double inv_d = band ? P.store[9 * (int64_t)band_idx_b(P, rid, x, y, z) + 8] : d[7][0];
             double Lq[7];
@@ -312,33 +415,41 @@ __global__ void __launch_bounds__(BW * 32, 2) k_batch_bwd(PlanDev P, BatchArgs A
             Lq[4] = lq_b(P, 4, x, y - 1, z + 1, d[4][0]);
             Lq[5] = lq_b(P, 5, x, y, z + 1, d[5][0]);
             Lq[6] = lq_b(P, 6, x - 1, y, z + 1, d[6][0]);
-            double v = EXACT ? dmul(inv_d, wf) : inv_d * wf;
+            double v = EXACT ? dmul(inv_d, c_wf) : inv_d * c_wf;
             if (EXACT) {  // reference order (_kernels.py:404-425)
                 v = msub<true>(v, Lq[0], wprev);
                 v = msub<true>(v, Lq[1], wn_hi);
-                v = msub<true>(v, Lq[2], wn_lo);
+                v = msub<true>(v, Lq[2], c_wn);
                 v = msub<true>(v, Lq[3], wts_hi);
-                v = msub<true>(v, Lq[4], wts_lo);
+                v = msub<true>(v, Lq[4], c_wts);
                 v = msub<true>(v, Lq[5], wtc_hi);
-                v = msub<true>(v, Lq[6], wtc_lo);
+                v = msub<true>(v, Lq[6], c_wtc);
             } else {
                 v = msub<false>(v, Lq[1], wn_hi);
-                v = msub<false>(v, Lq[2], wn_lo);
+                v = msub<false>(v, Lq[2], c_wn);
                 v = msub<false>(v, Lq[3], wts_hi);
-                v = msub<false>(v, Lq[4], wts_lo);
+                v = msub<false>(v, Lq[4], c_wts);
                 v = msub<false>(v, Lq[5], wtc_hi);
-                v = msub<false>(v, Lq[6], wtc_lo);
+                v = msub<false>(v, Lq[6], c_wtc);
                 v = msub<false>(v, Lq[0], wprev);
             }
             w[oc + X] = v;
-            u[oc + X] = dadd(uo, v);
+            u[oc + X] = dadd(c_u, v);
 #pragma unroll
             for (int mm = 0; mm < 8; ++mm) march<K>(d[mm]);
-            wn_hi = wn_lo;
-            wts_hi = wts_lo;
-            wtc_hi = wtc_lo;
+            wn_hi = c_wn;
+            wts_hi = c_wts;
+            wtc_hi = c_wtc;
             wprev = v;
-            if (x == 1) y -= BW;
+            c_wn = n_wn;
+            c_wts = n_wts;
+            c_wtc = n_wtc;
+            c_wf = n_wf;
+            c_u = n_u;
+            if (x == 1) {
+                y = A.rows[rid].prev;
+                if (y) bstart = A.Tmax - (A.rows[row_id(n, z, y)].start + (n - 1 - z - y) - 1);
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) {

@@ -2,17 +2,24 @@
 #pragma once
 #include <stdint.h>
 
+#include <vector>
+
 namespace tilu {
 
-constexpr int BW = 8;  // warps per CTA = rows of one z-layer in flight
+constexpr int BW = 8;        // warps per CTA = rows of one z-layer in flight
+constexpr int BWIN = 4;      // synchronisation window (steps between CTA barriers)
+constexpr int AMIN = BWIN + 2;  // min. start offset of consecutive rows of a layer (window + prefetch)
 
-// Per z-layer forward schedule: point (x, y) runs at global step O + A*(y-1) + x - 1.
+// Per-row schedule (indexed by row_id(n, z, y)): the forward step of point (x, y, z) is
+// start + x - 1; next / prev = the neighbouring rows (same layer) owned by the same warp, 0 = none.
+struct RowSched {
+    int start, next, prev;
+};
+
+// Per z-layer: first / last forward step and each warp's first / last row (0 = none).
 struct LayerSched {
-    int A;   // row skew (>= 2, A * BW >= longest row)
-    int B;   // synchronisation window = A - 1 steps
-    int O;   // step of the layer's first point
-    int T0;  // first step (= O)
-    int T1;  // last step
+    int T0, T1;
+    int first[BW], last[BW];
 };
 
 struct BatchArgs {
@@ -21,10 +28,14 @@ struct BatchArgs {
     double *w;        // packed scratch, zero on the lattice boundary
     int G, ntets;
     const LayerSched *sched;  // [n-3]
+    const RowSched *rows;     // [nrows]
     int Tmax, D;
-    int *flags;   // [G][n-3] progress counters (-1 = nothing done)
-    int *ticket;  // CTA ticket counter (starts at -1)
-    double *part; // [G][n-3][32] residual partial sums or nullptr
+    int *flags;    // [G][n-3] progress counters (-1 = nothing done)
+    int *ticket;   // CTA ticket counter (starts at -1)
+    double *part;  // [G][n-3][32] residual partial sums or nullptr
 };
+
+// Host: greedy list schedule of one level (tilu_batch.cu header comment).
+void batch_schedule(int n, std::vector<LayerSched> &layers, std::vector<RowSched> &rows, int &Tmax, int &D);
 
 }  // namespace tilu

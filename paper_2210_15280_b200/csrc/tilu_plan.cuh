@@ -40,6 +40,7 @@ struct tilu_plan {
     tilu::PlanDev dev;
     // batched (packed) path schedule
     const void *bsched;  // device LayerSched[n-3]
+    const void *brows;   // device RowSched[nrows]
     int bTmax, bD;
     int flags;
     int64_t interior;

@@ -1,7 +1,8 @@
-"""CPU verification of the batched path's wavefront schedule exactly as libtilu computes it:
-every lower-neighbour dependency is produced early enough (same row: 1 step; same layer: a
-full synchronisation window; layer below: D + 1 steps), a warp owns one row at a time, and
-the window-by-window progress handoff completes (no deadlock) forward and backward."""
+"""CPU verification of the batched path's greedy wavefront schedule exactly as libtilu
+computes it (tilu_batch_schedule): every value a point reads -- including the one-point-ahead
+prefetch -- was produced in a synchronisation window already closed (same layer) or covered by
+the progress counter the window waits for (layer below); rows of one warp never overlap; the
+window-by-window progress handoff completes forward and backward (no deadlock)."""
 
 import numpy as np
 import pytest
@@ -9,56 +10,79 @@ import pytest
 from paper_2210_15280_b200 import _lib
 
 LOWER = [(-1, 0, 0), (0, -1, 0), (1, -1, 0), (-1, 1, -1), (0, 1, -1), (0, 0, -1), (1, 0, -1)]
-BW = 8
+BWIN = 4
 
 
-def steps(level):
+def row_id(n, z, y):
+    return (z - 1) * (n - 2) - (z - 1) * z // 2 + (y - 1)
+
+
+def schedule(level):
     s = _lib.batch_schedule(level)
     n = 2 ** level
     T = {}
-    for zi in range(n - 3):
-        z = zi + 1
+    for z in range(1, n - 2):
         for y in range(1, n - 1 - z):
+            st = int(s["start"][row_id(n, z, y)])
             for x in range(1, n - z - y):
-                T[(x, y, z)] = int(s["O"][zi] + s["A"][zi] * (y - 1) + x - 1)
-    return s, T
+                T[(x, y, z)] = st + x - 1
+    T0 = {z: min(int(s["start"][row_id(n, z, y)]) for y in range(1, n - 1 - z)) for z in range(1, n - 2)}
+    return s, T, T0
+
+
+def window_start(t, t0):
+    return t0 + ((t - t0) // BWIN) * BWIN
 
 
 @pytest.mark.parametrize("level", [2, 3, 4, 5, 6])
-def test_dependencies_respected(level):
-    s, T = steps(level)
+def test_forward_reads_are_safe(level):
+    s, T, T0 = schedule(level)
+    n = 2 ** level
     D = s["D"]
     for (x, y, z), t in T.items():
+        # the values of point p are loaded at t (row start) or prefetched at t - 1
+        load_t = t if x == 1 else t - 1
+        ws = window_start(load_t, T0[z])
         for dx, dy, dz in LOWER:
             q = (x + dx, y + dy, z + dz)
             if q not in T:
                 continue
-            lag = t - T[q]
+            tq = T[q]
             if dz == 0 and dy == 0:
-                assert lag >= 1
+                assert tq == t - 1                      # own row: register
             elif dz == 0:
-                assert lag >= s["B"][z - 1], ((x, y, z), q)
+                assert tq < ws, ((x, y, z), q)          # closed window of this CTA
             else:
-                assert lag >= D + 1, ((x, y, z), q)
-    assert max(T.values()) == s["Tmax"]
+                need = min(ws + BWIN - 1 - D, int(s["T1"][z - 2]))
+                assert tq <= need, ((x, y, z), q)       # covered by the progress wait
 
 
 @pytest.mark.parametrize("level", [3, 5, 7, 9])
-def test_one_row_per_warp(level):
+def test_warps_own_one_row_at_a_time(level):
     s = _lib.batch_schedule(level)
     n = 2 ** level
-    for zi in range(n - 3):
-        R = n - 2 - (zi + 1)
-        assert s["A"][zi] >= 2 and s["A"][zi] * BW >= R and s["B"][zi] == s["A"][zi] - 1
+    for z in range(1, n - 2):
+        busy = {}
+        for y in range(1, n - 1 - z):
+            r = row_id(n, z, y)
+            w, st, m = int(s["warp"][r]), int(s["start"][r]), n - 1 - z - y
+            assert 0 <= w < 8
+            assert st >= busy.get(w, -1), (z, y)
+            busy[w] = st + m
+            if y > 1:
+                assert st >= int(s["start"][r - 1]) + BWIN + 2
 
 
-def _simulate(s, n, backward):
+def _simulate(level, backward):
+    s, _, T0 = schedule(level)
+    n = 2 ** level
     nl = n - 3
     Tmax, D = s["Tmax"], s["D"]
-    lo = [int(Tmax - s["T1"][z]) if backward else int(s["O"][z]) for z in range(nl)]
-    hi = [int(Tmax - s["O"][z]) if backward else int(s["T1"][z]) for z in range(nl)]
-    prog, pos, done = [-1] * nl, list(lo), set()
-    order = range(nl - 1, -1, -1) if backward else range(nl)
+    T1 = {z: int(s["T1"][z - 1]) for z in range(1, n - 2)}
+    lo = {z: (Tmax - T1[z] if backward else T0[z]) for z in T1}
+    hi = {z: (Tmax - T0[z] if backward else T1[z]) for z in T1}
+    prog, pos, done = {z: -1 for z in T1}, dict(lo), set()
+    order = range(nl, 0, -1) if backward else range(1, nl + 1)
     moved = True
     while moved:
         moved = False
@@ -66,19 +90,45 @@ def _simulate(s, n, backward):
             if z in done:
                 continue
             dep = z + 1 if backward else z - 1
-            B = int(s["B"][z])
-            if 0 <= dep < nl and prog[dep] < min(pos[z] + B - 2 - D, hi[dep]):
+            if dep in T1 and prog[dep] < min(pos[z] + BWIN - 1 - D, hi[dep]):
                 continue
-            t1 = min(pos[z] + B, hi[z] + 1)
+            t1 = min(pos[z] + BWIN, hi[z] + 1)
             prog[z], pos[z], moved = t1 - 1, t1, True
             if t1 > hi[z]:
                 done.add(z)
     return len(done) == nl
 
 
-@pytest.mark.parametrize("level", [2, 3, 4, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("level", [2, 3, 4, 5, 6, 7, 8])
 def test_handoff_completes(level):
-    s = _lib.batch_schedule(level)
+    assert _simulate(level, backward=False)
+    assert _simulate(level, backward=True)
+
+
+UPPER_READS = [(1, 0, 0), (0, 1, 0), (-1, 1, 0), (1, -1, 1), (0, -1, 1), (0, 0, 1), (-1, 0, 1)]
+
+
+@pytest.mark.parametrize("level", [2, 3, 4, 5, 6])
+def test_backward_reads_are_safe(level):
+    """Backward = time reversal: point p runs at Tmax - T(p) and reads its upper neighbours."""
+    s, T, T0 = schedule(level)
     n = 2 ** level
-    assert _simulate(s, n, backward=False)
-    assert _simulate(s, n, backward=True)
+    D, Tmax = s["D"], s["Tmax"]
+    T1 = {z: int(s["T1"][z - 1]) for z in range(1, n - 2)}
+    for (x, y, z), t in T.items():
+        tb = Tmax - t
+        m = n - 1 - z - y
+        load_t = tb if x == m else tb - 1
+        ws = window_start(load_t, Tmax - T1[z])
+        for dx, dy, dz in UPPER_READS:
+            q = (x + dx, y + dy, z + dz)
+            if q not in T:
+                continue
+            tq = Tmax - T[q]
+            if dz == 0 and dy == 0:
+                assert tq == tb - 1
+            elif dz == 0:
+                assert tq < ws, ((x, y, z), q)
+            else:
+                need = min(ws + BWIN - 1 - D, Tmax - T0[z + 1])
+                assert tq <= need, ((x, y, z), q)
