@@ -58,6 +58,26 @@ __device__ __forceinline__ void wait_progress(const int *flag, int need)
     }
 }
 
+// The sync warp (warp BW) of a CTA: window by window it publishes the CTA's progress (fence +
+// release, after the barrier that closes the window) and makes sure the data the NEXT window
+// reads from the neighbouring layer is published before it arrives at the barrier that opens it.
+// Compute warps only ever meet it at that one barrier per window.
+__device__ __forceinline__ void sync_warp_loop(int *myflag, const int *dep, int depEnd, int D, int t0, int t1)
+{
+    const bool leader = (threadIdx.x & 31) == 0;
+    if (leader && dep) wait_progress(dep, min(t0 + BWIN - 1 - D, depEnd));
+    __syncthreads();  // opens the first window
+    for (int tau0 = t0; tau0 <= t1; tau0 += BWIN) {
+        const int tau1 = min(tau0 + BWIN, t1 + 1);
+        if (leader && dep && tau1 <= t1) wait_progress(dep, min(tau1 + BWIN - 1 - D, depEnd));
+        __syncthreads();  // closes this window / opens the next
+        if (leader) {
+            __threadfence();
+            st_release(myflag, tau1 - 1);
+        }
+    }
+}
+
 __device__ __forceinline__ bool in_band_b(int x, int y, int z, int xe) { return z == 1 || y == 1 || x == 1 || x == xe; }
 __device__ __forceinline__ int band_idx_b(const PlanDev &P, int row, int x, int y, int z)
 {
@@ -129,7 +149,7 @@ void batch_schedule(int n, std::vector<LayerSched> &layers, std::vector<RowSched
 // forward: residual + L solve
 // ----------------------------------------------------------------------------------------------
 template <int K, bool EXACT, bool CONST_ROW>
-__global__ void __launch_bounds__(BW * 32, 1) k_batch_fwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
 {
     __shared__ int s_ticket;
     __shared__ double s_red[BW][32];
@@ -165,11 +185,13 @@ __global__ void __launch_bounds__(BW * 32, 1) k_batch_fwd(PlanDev P, BatchArgs A
     double c_ue = 0, c_us = 0, c_un = 0, c_ubn = 0, c_ubc = 0, c_uts = 0, c_utc = 0, c_f = 0;
     double c_ws = 0, c_wbn = 0, c_wbc = 0;
     double ss = 0.0;
+    if (warp == BW) {
+        sync_warp_loop(myflag, below, belowT1, A.D, T0, T1);
+        ss = 0.0;
+    } else {
     if (y) start = A.rows[row_id(n, z, y)].start;
-
+    __syncthreads();  // first window opened by the sync warp
     for (int tau0 = T0; tau0 <= T1; tau0 += BWIN) {
-        if (threadIdx.x == 0 && below) wait_progress(below, min(tau0 + BWIN - 1 - A.D, belowT1));
-        __syncthreads();
         const int tau1 = min(tau0 + BWIN, T1 + 1);
         for (int tau = tau0; tau < tau1; ++tau) {
             if (!y) break;
@@ -316,13 +338,10 @@ __global__ void __launch_bounds__(BW * 32, 1) k_batch_fwd(PlanDev P, BatchArgs A
             }
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            st_release(myflag, tau1 - 1);
-        }
+    }
     }
     if (A.part) {
-        s_red[warp][lane] = ss;
+        if (warp < BW) s_red[warp][lane] = ss;
         __syncthreads();
         if (warp == 0) {
             double t = 0.0;
@@ -337,7 +356,7 @@ __global__ void __launch_bounds__(BW * 32, 1) k_batch_fwd(PlanDev P, BatchArgs A
 // backward: D^{-1} + L^T solve + update, exact time reversal of the forward schedule
 // ----------------------------------------------------------------------------------------------
 template <int K, bool EXACT>
-__global__ void __launch_bounds__(BW * 32, 1) k_batch_bwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
 {
     __shared__ int s_ticket;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -361,11 +380,13 @@ __global__ void __launch_bounds__(BW * 32, 1) k_batch_bwd(PlanDev P, BatchArgs A
     double d[8][K];
     double wn_hi = 0, wts_hi = 0, wtc_hi = 0, wprev = 0;
     double c_wn = 0, c_wts = 0, c_wtc = 0, c_wf = 0, c_u = 0;
+    if (warp == BW) {
+        sync_warp_loop(myflag, above, aboveEnd, A.D, tb0, tb1);
+        return;
+    }
     if (y) bstart = A.Tmax - (A.rows[row_id(n, z, y)].start + (n - 1 - z - y) - 1);
-
+    __syncthreads();  // first window opened by the sync warp
     for (int tau0 = tb0; tau0 <= tb1; tau0 += BWIN) {
-        if (threadIdx.x == 0 && above) wait_progress(above, min(tau0 + BWIN - 1 - A.D, aboveEnd));
-        __syncthreads();
         const int tau1 = min(tau0 + BWIN, tb1 + 1);
         for (int tau = tau0; tau < tau1; ++tau) {
             if (!y) break;
@@ -452,10 +473,6 @@ __global__ void __launch_bounds__(BW * 32, 1) k_batch_bwd(PlanDev P, BatchArgs A
             }
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            st_release(myflag, tau1 - 1);
-        }
     }
 }
 
@@ -538,11 +555,11 @@ static void launch_fwd_k(const PlanDev &P, const BatchArgs &A, bool exact, cudaS
     const unsigned grid = (unsigned)(A.G * (P.n - 3));
     const bool c = P.arow != nullptr;
     if (exact) {
-        if (c) k_batch_fwd<K, true, true><<<grid, BW * 32, 0, s>>>(P, A);
-        else k_batch_fwd<K, true, false><<<grid, BW * 32, 0, s>>>(P, A);
+        if (c) k_batch_fwd<K, true, true><<<grid, NT, 0, s>>>(P, A);
+        else k_batch_fwd<K, true, false><<<grid, NT, 0, s>>>(P, A);
     } else {
-        if (c) k_batch_fwd<K, false, true><<<grid, BW * 32, 0, s>>>(P, A);
-        else k_batch_fwd<K, false, false><<<grid, BW * 32, 0, s>>>(P, A);
+        if (c) k_batch_fwd<K, false, true><<<grid, NT, 0, s>>>(P, A);
+        else k_batch_fwd<K, false, false><<<grid, NT, 0, s>>>(P, A);
     }
 }
 
@@ -550,8 +567,8 @@ template <int K>
 static void launch_bwd_k(const PlanDev &P, const BatchArgs &A, bool exact, cudaStream_t s)
 {
     const unsigned grid = (unsigned)(A.G * (P.n - 3));
-    if (exact) k_batch_bwd<K, true><<<grid, BW * 32, 0, s>>>(P, A);
-    else k_batch_bwd<K, false><<<grid, BW * 32, 0, s>>>(P, A);
+    if (exact) k_batch_bwd<K, true><<<grid, NT, 0, s>>>(P, A);
+    else k_batch_bwd<K, false><<<grid, NT, 0, s>>>(P, A);
 }
 
 bool launch_batch_pass(const PlanDev &P, const BatchArgs &A, bool exact, bool fwd, cudaStream_t s)

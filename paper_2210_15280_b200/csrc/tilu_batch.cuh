@@ -6,8 +6,9 @@
 
 namespace tilu {
 
-constexpr int BW = 8;        // warps per CTA = rows of one z-layer in flight
-constexpr int BWIN = 4;      // synchronisation window (steps between CTA barriers)
+constexpr int BW = 8;        // compute warps per CTA = rows of one z-layer in flight
+constexpr int NT = (BW + 1) * 32;  // + one sync warp (progress wait / publish off the compute path)
+constexpr int BWIN = 8;      // synchronisation window (steps between CTA barriers)
 constexpr int AMIN = BWIN + 2;  // min. start offset of consecutive rows of a layer (window + prefetch)
 
 // Per-row schedule (indexed by row_id(n, z, y)): the forward step of point (x, y, z) is

@@ -10,7 +10,7 @@ import pytest
 from paper_2210_15280_b200 import _lib
 
 LOWER = [(-1, 0, 0), (0, -1, 0), (1, -1, 0), (-1, 1, -1), (0, 1, -1), (0, 0, -1), (1, 0, -1)]
-BWIN = 4
+BWIN = 8  # tilu_batch.cuh
 
 
 def row_id(n, z, y):
