@@ -3,6 +3,7 @@
 // point returns a status code and records a thread-local message.
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -165,6 +166,7 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
     A.rows = static_cast<const RowSched *>(p->brows);
     A.Tmax = p->bTmax;
     A.D = p->bD;
+    A.bwin = p->bwin;
     for (int k = 0; k < sweeps; ++k) {
         cudaMemsetAsync(sync, 0xFF, nsync * sizeof(int), s);
         A.ticket = sync;
@@ -376,7 +378,10 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
         std::vector<LayerSched> sch;
         std::vector<RowSched> rsch;
         int T = 0, D = 0;
-        batch_schedule(n, sch, rsch, T, D);
+        const char *ev = std::getenv("TILU_BWIN");
+        const int bwin = ev ? std::max(1, std::min(64, std::atoi(ev))) : BWIN_DEFAULT;
+        batch_schedule(n, bwin, sch, rsch, T, D);
+        p->bwin = bwin;
         LayerSched *dsch = nullptr;
         RowSched *drs = nullptr;
         if ((rc = dev_upload(p, &dsch, sch.data(), sch.size())) || (rc = dev_upload(p, &drs, rsch.data(), rsch.size()))) {
@@ -521,13 +526,14 @@ static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int nt
     return check_cuda("sweep");
 }
 
-int tilu_batch_schedule(int level, int *row_start, int *row_warp, int *layer_T1, int *D, int *Tmax)
+int tilu_batch_schedule(int level, int bwin, int *row_start, int *row_warp, int *layer_T1, int *D, int *Tmax)
 {
     if (level < 2 || level > 10) return -fail(TILU_EINVAL, "level %d outside 2..10", level);
+    if (bwin < 1 || bwin > 64) return -fail(TILU_EINVAL, "window %d outside 1..64", bwin);
     const int n = 1 << level;
     std::vector<LayerSched> sch;
     std::vector<RowSched> rs;
-    batch_schedule(n, sch, rs, *Tmax, *D);
+    batch_schedule(n, bwin, sch, rs, *Tmax, *D);
     for (int z = 1; z <= n - 3; ++z) {
         layer_T1[z - 1] = sch[z - 1].T1;
         for (int wi = 0; wi < BW; ++wi)

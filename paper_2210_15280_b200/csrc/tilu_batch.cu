@@ -35,10 +35,15 @@
 
 namespace tilu {
 
-__device__ __forceinline__ int ld_acquire(const int *p)
+// Progress counters are polled with relaxed gpu-scope loads: ld.acquire.gpu would emit
+// CCTL.IVALL (invalidate the SM's whole L1) on every poll and wipe the u-reuse the compute warps
+// rely on.  No acquire is needed for correctness here: a consumer never touches a w line before
+// its producer wrote it (dependency order), so L1 cannot hold a stale copy, and the consumer's
+// data loads are issued only after the flag value has returned (control dependency + bar.sync).
+__device__ __forceinline__ int ld_relaxed(const int *p)
 {
     int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release(int *p, int v)
@@ -52,7 +57,7 @@ __device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
 __device__ __forceinline__ void wait_progress(const int *flag, int need)
 {
     long long polls = 0;
-    while (ld_acquire(flag) < need) {
+    while (ld_relaxed(flag) < need) {
         __nanosleep(64);
         if (++polls > (1ll << 27)) __trap();
     }
@@ -62,19 +67,17 @@ __device__ __forceinline__ void wait_progress(const int *flag, int need)
 // release, after the barrier that closes the window) and makes sure the data the NEXT window
 // reads from the neighbouring layer is published before it arrives at the barrier that opens it.
 // Compute warps only ever meet it at that one barrier per window.
-__device__ __forceinline__ void sync_warp_loop(int *myflag, const int *dep, int depEnd, int D, int t0, int t1)
+__device__ __forceinline__ void sync_warp_loop(int *myflag, const int *dep, int depEnd, int D, int t0, int t1,
+                                               int bwin)
 {
     const bool leader = (threadIdx.x & 31) == 0;
-    if (leader && dep) wait_progress(dep, min(t0 + BWIN - 1 - D, depEnd));
+    if (leader && dep) wait_progress(dep, min(t0 + bwin - 1 - D, depEnd));
     __syncthreads();  // opens the first window
-    for (int tau0 = t0; tau0 <= t1; tau0 += BWIN) {
-        const int tau1 = min(tau0 + BWIN, t1 + 1);
-        if (leader && dep && tau1 <= t1) wait_progress(dep, min(tau1 + BWIN - 1 - D, depEnd));
+    for (int tau0 = t0; tau0 <= t1; tau0 += bwin) {
+        const int tau1 = min(tau0 + bwin, t1 + 1);
+        if (leader && dep && tau1 <= t1) wait_progress(dep, min(tau1 + bwin - 1 - D, depEnd));
         __syncthreads();  // closes this window / opens the next
-        if (leader) {
-            __threadfence();
-            st_release(myflag, tau1 - 1);
-        }
+        if (leader) st_release(myflag, tau1 - 1);  // MEMBAR.GPU + store: cumulative over the barrier
     }
 }
 
@@ -98,10 +101,11 @@ __device__ __forceinline__ double lq_b(const PlanDev &P, int m, int qx, int qy, 
 // ----------------------------------------------------------------------------------------------
 // host: greedy list schedule
 // ----------------------------------------------------------------------------------------------
-void batch_schedule(int n, std::vector<LayerSched> &layers, std::vector<RowSched> &rows, int &Tmax, int &D)
+void batch_schedule(int n, int bwin, std::vector<LayerSched> &layers, std::vector<RowSched> &rows, int &Tmax, int &D)
 {
     const int nl = n - 3;
-    D = 2 * BWIN + 2;
+    const int amin = bwin + 2;
+    D = 2 * bwin + 2;
     layers.assign(nl, LayerSched{});
     rows.assign((size_t)(n - 3) * (n - 2) / 2 + 1, RowSched{0, 0, 0});
     Tmax = 0;
@@ -119,7 +123,7 @@ void batch_schedule(int n, std::vector<LayerSched> &layers, std::vector<RowSched
         L.T1 = 0;
         for (int y = 1; y <= R; ++y) {
             const int m = n - 1 - z - y;
-            int t = std::max(0, prev_start + AMIN);
+            int t = std::max(0, prev_start + amin);
             if (z > 1) {
                 t = std::max(t, rows[row_id(n, z - 1, y + 1)].start + 1 + D);
                 t = std::max(t, rows[row_id(n, z - 1, y)].start + 2 + D);
@@ -186,13 +190,13 @@ __global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
     double c_ws = 0, c_wbn = 0, c_wbc = 0;
     double ss = 0.0;
     if (warp == BW) {
-        sync_warp_loop(myflag, below, belowT1, A.D, T0, T1);
+        sync_warp_loop(myflag, below, belowT1, A.D, T0, T1, A.bwin);
         ss = 0.0;
     } else {
     if (y) start = A.rows[row_id(n, z, y)].start;
     __syncthreads();  // first window opened by the sync warp
-    for (int tau0 = T0; tau0 <= T1; tau0 += BWIN) {
-        const int tau1 = min(tau0 + BWIN, T1 + 1);
+    for (int tau0 = T0; tau0 <= T1; tau0 += A.bwin) {
+        const int tau1 = min(tau0 + A.bwin, T1 + 1);
         for (int tau = tau0; tau < tau1; ++tau) {
             if (!y) break;
             const int x = tau - start + 1;
@@ -381,13 +385,13 @@ __global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
     double wn_hi = 0, wts_hi = 0, wtc_hi = 0, wprev = 0;
     double c_wn = 0, c_wts = 0, c_wtc = 0, c_wf = 0, c_u = 0;
     if (warp == BW) {
-        sync_warp_loop(myflag, above, aboveEnd, A.D, tb0, tb1);
+        sync_warp_loop(myflag, above, aboveEnd, A.D, tb0, tb1, A.bwin);
         return;
     }
     if (y) bstart = A.Tmax - (A.rows[row_id(n, z, y)].start + (n - 1 - z - y) - 1);
     __syncthreads();  // first window opened by the sync warp
-    for (int tau0 = tb0; tau0 <= tb1; tau0 += BWIN) {
-        const int tau1 = min(tau0 + BWIN, tb1 + 1);
+    for (int tau0 = tb0; tau0 <= tb1; tau0 += A.bwin) {
+        const int tau1 = min(tau0 + A.bwin, tb1 + 1);
         for (int tau = tau0; tau < tau1; ++tau) {
             if (!y) break;
             const int k = tau - bstart;  // 0-based position along the descending row

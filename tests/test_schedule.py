@@ -10,15 +10,14 @@ import pytest
 from paper_2210_15280_b200 import _lib
 
 LOWER = [(-1, 0, 0), (0, -1, 0), (1, -1, 0), (-1, 1, -1), (0, 1, -1), (0, 0, -1), (1, 0, -1)]
-BWIN = 8  # tilu_batch.cuh
 
 
 def row_id(n, z, y):
     return (z - 1) * (n - 2) - (z - 1) * z // 2 + (y - 1)
 
 
-def schedule(level):
-    s = _lib.batch_schedule(level)
+def schedule(level, bwin):
+    s = _lib.batch_schedule(level, bwin)
     n = 2 ** level
     T = {}
     for z in range(1, n - 2):
@@ -30,19 +29,20 @@ def schedule(level):
     return s, T, T0
 
 
-def window_start(t, t0):
-    return t0 + ((t - t0) // BWIN) * BWIN
+def window_start(t, t0, bwin):
+    return t0 + ((t - t0) // bwin) * bwin
 
 
+@pytest.mark.parametrize("bwin", [1, 2, 8])
 @pytest.mark.parametrize("level", [2, 3, 4, 5, 6])
-def test_forward_reads_are_safe(level):
-    s, T, T0 = schedule(level)
+def test_forward_reads_are_safe(level, bwin):
+    s, T, T0 = schedule(level, bwin)
     n = 2 ** level
     D = s["D"]
     for (x, y, z), t in T.items():
         # the values of point p are loaded at t (row start) or prefetched at t - 1
         load_t = t if x == 1 else t - 1
-        ws = window_start(load_t, T0[z])
+        ws = window_start(load_t, T0[z], bwin)
         for dx, dy, dz in LOWER:
             q = (x + dx, y + dy, z + dz)
             if q not in T:
@@ -53,13 +53,14 @@ def test_forward_reads_are_safe(level):
             elif dz == 0:
                 assert tq < ws, ((x, y, z), q)          # closed window of this CTA
             else:
-                need = min(ws + BWIN - 1 - D, int(s["T1"][z - 2]))
+                need = min(ws + bwin - 1 - D, int(s["T1"][z - 2]))
                 assert tq <= need, ((x, y, z), q)       # covered by the progress wait
 
 
+@pytest.mark.parametrize("bwin", [2, 8])
 @pytest.mark.parametrize("level", [3, 5, 7, 9])
-def test_warps_own_one_row_at_a_time(level):
-    s = _lib.batch_schedule(level)
+def test_warps_own_one_row_at_a_time(level, bwin):
+    s = _lib.batch_schedule(level, bwin)
     n = 2 ** level
     for z in range(1, n - 2):
         busy = {}
@@ -70,11 +71,11 @@ def test_warps_own_one_row_at_a_time(level):
             assert st >= busy.get(w, -1), (z, y)
             busy[w] = st + m
             if y > 1:
-                assert st >= int(s["start"][r - 1]) + BWIN + 2
+                assert st >= int(s["start"][r - 1]) + bwin + 2
 
 
-def _simulate(level, backward):
-    s, _, T0 = schedule(level)
+def _simulate(level, backward, bwin):
+    s, _, T0 = schedule(level, bwin)
     n = 2 ** level
     nl = n - 3
     Tmax, D = s["Tmax"], s["D"]
@@ -90,28 +91,30 @@ def _simulate(level, backward):
             if z in done:
                 continue
             dep = z + 1 if backward else z - 1
-            if dep in T1 and prog[dep] < min(pos[z] + BWIN - 1 - D, hi[dep]):
+            if dep in T1 and prog[dep] < min(pos[z] + bwin - 1 - D, hi[dep]):
                 continue
-            t1 = min(pos[z] + BWIN, hi[z] + 1)
+            t1 = min(pos[z] + bwin, hi[z] + 1)
             prog[z], pos[z], moved = t1 - 1, t1, True
             if t1 > hi[z]:
                 done.add(z)
     return len(done) == nl
 
 
+@pytest.mark.parametrize("bwin", [1, 2, 8])
 @pytest.mark.parametrize("level", [2, 3, 4, 5, 6, 7, 8])
-def test_handoff_completes(level):
-    assert _simulate(level, backward=False)
-    assert _simulate(level, backward=True)
+def test_handoff_completes(level, bwin):
+    assert _simulate(level, backward=False, bwin=bwin)
+    assert _simulate(level, backward=True, bwin=bwin)
 
 
 UPPER_READS = [(1, 0, 0), (0, 1, 0), (-1, 1, 0), (1, -1, 1), (0, -1, 1), (0, 0, 1), (-1, 0, 1)]
 
 
+@pytest.mark.parametrize("bwin", [1, 2, 8])
 @pytest.mark.parametrize("level", [2, 3, 4, 5, 6])
-def test_backward_reads_are_safe(level):
+def test_backward_reads_are_safe(level, bwin):
     """Backward = time reversal: point p runs at Tmax - T(p) and reads its upper neighbours."""
-    s, T, T0 = schedule(level)
+    s, T, T0 = schedule(level, bwin)
     n = 2 ** level
     D, Tmax = s["D"], s["Tmax"]
     T1 = {z: int(s["T1"][z - 1]) for z in range(1, n - 2)}
@@ -119,7 +122,7 @@ def test_backward_reads_are_safe(level):
         tb = Tmax - t
         m = n - 1 - z - y
         load_t = tb if x == m else tb - 1
-        ws = window_start(load_t, Tmax - T1[z])
+        ws = window_start(load_t, Tmax - T1[z], bwin)
         for dx, dy, dz in UPPER_READS:
             q = (x + dx, y + dy, z + dz)
             if q not in T:
@@ -130,5 +133,5 @@ def test_backward_reads_are_safe(level):
             elif dz == 0:
                 assert tq < ws, ((x, y, z), q)
             else:
-                need = min(ws + BWIN - 1 - D, Tmax - T0[z + 1])
+                need = min(ws + bwin - 1 - D, Tmax - T0[z + 1])
                 assert tq <= need, ((x, y, z), q)
