@@ -167,6 +167,7 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
     A.Tmax = p->bTmax;
     A.D = p->bD;
     A.bwin = p->bwin;
+    std::memcpy(A.arow, p->harow, sizeof(A.arow));
     for (int k = 0; k < sweeps; ++k) {
         cudaMemsetAsync(sync, 0xFF, nsync * sizeof(int), s);
         A.ticket = sync;
@@ -346,6 +347,7 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
         tilu_plan_destroy(p);
         return rc;
     }
+    if (d->arow) std::memcpy(p->harow, d->arow, sizeof(p->harow));
     if (d->arow && (rc = dev_upload(p, &darow, d->arow, 15))) {
         tilu_plan_destroy(p);
         return rc;

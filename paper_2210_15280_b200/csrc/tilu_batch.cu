@@ -150,18 +150,62 @@ void batch_schedule(int n, int bwin, std::vector<LayerSched> &layers, std::vecto
 }
 
 // ----------------------------------------------------------------------------------------------
+// Shared NDDF tables: every lane of a warp works on a different tet of the SAME lattice row and
+// all tets share the surrogate, so the forward-difference tables are identical across lanes.
+// They live once per warp in shared memory and one forward-difference step is done lane-parallel:
+// lane e updates entry e (d[m][j] += d[m][j+1]), reading all old values before any write --
+// the same unfused additions as the reference's serial march (_kernels.py:313-316), 28-32 lanes
+// busy instead of 28-32 dependent-free adds in every lane.
+// ----------------------------------------------------------------------------------------------
+template <int M, int K>
+__device__ __forceinline__ void smem_load_table(double *tab, const double *__restrict__ src, int lane)
+{
+    for (int e = lane; e < M * K; e += 32) tab[e] = src[e];
+    __syncwarp();
+}
+
+template <int M, int K>
+__device__ __forceinline__ void smem_march(double *tab, int lane)
+{
+    constexpr int NE = M * (K - 1);
+    if (NE == 0) return;
+    constexpr int IT = NE > 0 ? (NE + 31) / 32 : 1;
+    double nv[IT];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const int e = lane + 32 * i;
+        if (e < NE) {
+            const int m = e / (K - 1), j = e - m * (K - 1);
+            nv[i] = dadd(tab[m * K + j], tab[m * K + j + 1]);
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const int e = lane + 32 * i;
+        if (e < NE) {
+            const int m = e / (K - 1), j = e - m * (K - 1);
+            tab[m * K + j] = nv[i];
+        }
+    }
+    __syncwarp();
+}
+
+// ----------------------------------------------------------------------------------------------
 // forward: residual + L solve
 // ----------------------------------------------------------------------------------------------
 template <int K, bool EXACT, bool CONST_ROW>
-__global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
 {
     __shared__ int s_ticket;
     __shared__ double s_red[BW][32];
+    __shared__ double s_tab[BW][7 * K];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_ticket = atomicAdd(A.ticket, 1) + 1;  // counter starts at -1
     __syncthreads();
     const int nl = P.n - 3;
     const int zi = s_ticket / A.G, g = s_ticket - (s_ticket / A.G) * A.G;
+    double *tab = s_tab[warp < BW ? warp : 0];
     const int n = P.n, z = zi + 1;
     const int T0 = A.sched[zi].T0, T1 = A.sched[zi].T1;
     const size_t gb = (size_t)g * P.grid * 32 + lane;
@@ -172,16 +216,12 @@ __global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
     const int *below = z > 1 ? myflag - 1 : nullptr;
     const int belowT1 = z > 1 ? A.sched[zi - 1].T1 : 0;
 
-    double a[15];
-    if (CONST_ROW) {
-#pragma unroll
-        for (int i = 0; i < 15; ++i) a[i] = P.arow[i];
-    }
+    double ap[15];  // per-point stencil rows (non-constant operators)
+    const double *a = CONST_ROW ? A.arow : ap;
 
     int y = A.sched[zi].first[warp];
     int m = 0, rid = 0, start = 0;
     uint32_t oc = 0, os = 0, on = 0, obn = 0, obc = 0, ots = 0, otc = 0;
-    double d[7][K];
     // sliding windows: values of point x-1 / x that point x+1 reuses
     double u_wm = 0, u_c = 0, us0 = 0, un_m = 0, ubn_m = 0, ubc0 = 0, uts0 = 0, utc_m = 0;
     double ws0 = 0, wbn_m = 0, wbc0 = 0, wprev = 0;
@@ -211,11 +251,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
                 obc = (uint32_t)row_offset(n, z - 1, y) * 32u;
                 ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
                 otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
-                const double *sd = P.seedF + (int64_t)rid * 7 * K;
-#pragma unroll
-                for (int mm = 0; mm < 7; ++mm)
-#pragma unroll
-                    for (int j = 0; j < K; ++j) d[mm][j] = sd[mm * K + j];
+                smem_load_table<7, K>(tab, P.seedF + (int64_t)rid * 7 * K, lane);
                 u_wm = u[oc];
                 u_c = u[oc + 32];
                 us0 = u[os + 32];
@@ -261,7 +297,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
             if (!CONST_ROW) {
                 const double *ar = P.arows + 15 * (int64_t)(oc / 32u + x);
 #pragma unroll
-                for (int i = 0; i < 15; ++i) a[i] = ar[i];
+                for (int i = 0; i < 15; ++i) ap[i] = ar[i];
             }
             // residual in stencil_apply order (_kernels.py:255-266), then f - A u
             double acc = EXACT ? dmul(a[7], u_c) : a[7] * u_c;
@@ -289,7 +325,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
                 for (int mm = 0; mm < 7; ++mm) L[mm] = st[mm];
             } else {
 #pragma unroll
-                for (int mm = 0; mm < 7; ++mm) L[mm] = d[mm][0];
+                for (int mm = 0; mm < 7; ++mm) L[mm] = tab[mm * K];
             }
             double v;
             if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
@@ -310,8 +346,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
                 v = msub<false>(v, L[0], wprev);
             }
             w[oc + X] = v;
-#pragma unroll
-            for (int mm = 0; mm < 7; ++mm) march<K>(d[mm]);
+            smem_march<7, K>(tab, lane);
             // slide the windows
             u_wm = u_c;
             u_c = c_ue;
@@ -360,12 +395,14 @@ __global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
 // backward: D^{-1} + L^T solve + update, exact time reversal of the forward schedule
 // ----------------------------------------------------------------------------------------------
 template <int K, bool EXACT>
-__global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(NT, 2) k_batch_bwd(PlanDev P, BatchArgs A)
 {
     __shared__ int s_ticket;
+    __shared__ double s_tab[BW][8 * K];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_ticket = atomicAdd(A.ticket, 1) + 1;
     __syncthreads();
+    double *tab = s_tab[warp < BW ? warp : 0];
     const int nl = P.n - 3;
     const int li = s_ticket / A.G, g = s_ticket - li * A.G;
     const int zi = nl - 1 - li;
@@ -381,7 +418,6 @@ __global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
     int y = A.sched[zi].last[warp];
     int m = 0, rid = 0, bstart = 0;  // bstart: backward step of the row's first point (x = m)
     uint32_t oc = 0, on = 0, ots = 0, otc = 0;
-    double d[8][K];
     double wn_hi = 0, wts_hi = 0, wtc_hi = 0, wprev = 0;
     double c_wn = 0, c_wts = 0, c_wtc = 0, c_wf = 0, c_u = 0;
     if (warp == BW) {
@@ -403,11 +439,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
                 on = (uint32_t)row_offset(n, z, y + 1) * 32u;
                 ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
                 otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
-                const double *sd = P.seedB + (int64_t)rid * 8 * K;
-#pragma unroll
-                for (int mm = 0; mm < 8; ++mm)
-#pragma unroll
-                    for (int j = 0; j < K; ++j) d[mm][j] = sd[mm * K + j];
+                smem_load_table<8, K>(tab, P.seedB + (int64_t)rid * 8 * K, lane);
                 const uint32_t M = (uint32_t)m * 32u;
                 wn_hi = ldcg(w + on + M);
                 wts_hi = ldcg(w + ots + M + 32);
@@ -431,15 +463,15 @@ __global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
                 n_u = u[oc + X1];
             }
             const bool band = P.variant == 1 && in_band_b(x, y, z, m);
-            const double inv_d = band ? P.store[9 * (int64_t)band_idx_b(P, rid, x, y, z) + 8] : d[7][0];
+            const double inv_d = band ? P.store[9 * (int64_t)band_idx_b(P, rid, x, y, z) + 8] : tab[7 * K];
             double Lq[7];
-            Lq[0] = lq_b(P, 0, x + 1, y, z, d[0][0]);
-            Lq[1] = lq_b(P, 1, x, y + 1, z, d[1][0]);
-            Lq[2] = lq_b(P, 2, x - 1, y + 1, z, d[2][0]);
-            Lq[3] = lq_b(P, 3, x + 1, y - 1, z + 1, d[3][0]);
-            Lq[4] = lq_b(P, 4, x, y - 1, z + 1, d[4][0]);
-            Lq[5] = lq_b(P, 5, x, y, z + 1, d[5][0]);
-            Lq[6] = lq_b(P, 6, x - 1, y, z + 1, d[6][0]);
+            Lq[0] = lq_b(P, 0, x + 1, y, z, tab[0 * K]);
+            Lq[1] = lq_b(P, 1, x, y + 1, z, tab[1 * K]);
+            Lq[2] = lq_b(P, 2, x - 1, y + 1, z, tab[2 * K]);
+            Lq[3] = lq_b(P, 3, x + 1, y - 1, z + 1, tab[3 * K]);
+            Lq[4] = lq_b(P, 4, x, y - 1, z + 1, tab[4 * K]);
+            Lq[5] = lq_b(P, 5, x, y, z + 1, tab[5 * K]);
+            Lq[6] = lq_b(P, 6, x - 1, y, z + 1, tab[6 * K]);
             double v = EXACT ? dmul(inv_d, c_wf) : inv_d * c_wf;
             if (EXACT) {  // reference order (_kernels.py:404-425)
                 v = msub<true>(v, Lq[0], wprev);
@@ -460,8 +492,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
             }
             w[oc + X] = v;
             u[oc + X] = dadd(c_u, v);
-#pragma unroll
-            for (int mm = 0; mm < 8; ++mm) march<K>(d[mm]);
+            smem_march<8, K>(tab, lane);
             wn_hi = c_wn;
             wts_hi = c_wts;
             wtc_hi = c_wtc;

@@ -34,6 +34,7 @@ struct BatchArgs {
     int *flags;    // [G][n-3] progress counters (-1 = nothing done)
     int *ticket;   // CTA ticket counter (starts at -1)
     double *part;  // [G][n-3][32] residual partial sums or nullptr
+    double arow[15];  // constant stencil (kernel-parameter constant bank: DMUL operands, no registers)
 };
 
 // Host: greedy list schedule of one level (tilu_batch.cu header comment).

@@ -42,6 +42,7 @@ struct tilu_plan {
     const void *bsched;  // device LayerSched[n-3]
     const void *brows;   // device RowSched[nrows]
     int bTmax, bD, bwin;
+    double harow[15];  // host copy of the constant stencil (batched kernel parameters)
     int flags;
     int64_t interior;
     int64_t nband;
