@@ -156,7 +156,13 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
     double *part = rnorm2 ? sc.get((size_t)G * nl * 32) : nullptr;
     if (!sync || (rnorm2 && !part)) return fail(TILU_ENOMEM, "scratch allocation failed");
     const bool exact = !(p->flags & TILU_FAST);
+    // debug trace (TILU_TRACE=path): per CTA globaltimer stamps of the last sweep's passes
+    static const char *trace_path = std::getenv("TILU_TRACE");
+    unsigned long long *trace = nullptr;
+    const size_t ntrace = 2 * 4 * (size_t)G * nl;
+    if (trace_path) trace = reinterpret_cast<unsigned long long *>(sc.get(ntrace));
     BatchArgs A{};
+    A.trace = nullptr;
     A.u = up;
     A.f = fp;
     A.w = wp;
@@ -173,12 +179,14 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
         A.ticket = sync;
         A.flags = sync + 2;
         A.part = part;
+        A.trace = trace;
         prof_begin(s);
         bool ok = launch_batch_pass(P, A, exact, true, s);
         prof_end("batch_fwd", s);
         A.ticket = sync + 1;
         A.flags = sync + 2 + (size_t)G * nl;
         A.part = nullptr;
+        A.trace = trace ? trace + 4 * (size_t)G * nl : nullptr;
         prof_begin(s);
         ok = ok && launch_batch_pass(P, A, exact, false, s);
         prof_end("batch_bwd", s);
@@ -187,6 +195,17 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
         if (rnorm2) {
             launch_batch_norms(part, nl, ntets, rnorm2 + (int64_t)k * ntets, s);
             ++g_launches;
+        }
+    }
+    if (trace) {
+        std::vector<unsigned long long> h(ntrace);
+        cudaMemcpyAsync(h.data(), trace, ntrace * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (FILE *fh = std::fopen(trace_path, "wb")) {
+            const int hdr[3] = {G, nl, 4};
+            std::fwrite(hdr, sizeof(int), 3, fh);
+            std::fwrite(h.data(), sizeof(unsigned long long), ntrace, fh);
+            std::fclose(fh);
         }
     }
     return TILU_OK;

@@ -67,17 +67,35 @@ __device__ __forceinline__ void wait_progress(const int *flag, int need)
 // release, after the barrier that closes the window) and makes sure the data the NEXT window
 // reads from the neighbouring layer is published before it arrives at the barrier that opens it.
 // Compute warps only ever meet it at that one barrier per window.
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ void sync_warp_loop(int *myflag, const int *dep, int depEnd, int D, int t0, int t1,
-                                               int bwin)
+                                               int bwin, unsigned long long *trace)
 {
     const bool leader = (threadIdx.x & 31) == 0;
+    unsigned long long waited = 0;
+    if (trace && leader) trace[0] = gtimer();
     if (leader && dep) wait_progress(dep, min(t0 + bwin - 1 - D, depEnd));
+    if (trace && leader) trace[1] = gtimer();
     __syncthreads();  // opens the first window
     for (int tau0 = t0; tau0 <= t1; tau0 += bwin) {
         const int tau1 = min(tau0 + bwin, t1 + 1);
-        if (leader && dep && tau1 <= t1) wait_progress(dep, min(tau1 + bwin - 1 - D, depEnd));
+        if (leader && dep && tau1 <= t1) {
+            const unsigned long long a = trace ? gtimer() : 0;
+            wait_progress(dep, min(tau1 + bwin - 1 - D, depEnd));
+            if (trace) waited += gtimer() - a;
+        }
         __syncthreads();  // closes this window / opens the next
         if (leader) st_release(myflag, tau1 - 1);  // MEMBAR.GPU + store: cumulative over the barrier
+    }
+    if (trace && leader) {
+        trace[2] = gtimer();
+        trace[3] = waited;
     }
 }
 
@@ -230,7 +248,7 @@ __global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
     double c_ws = 0, c_wbn = 0, c_wbc = 0;
     double ss = 0.0;
     if (warp == BW) {
-        sync_warp_loop(myflag, below, belowT1, A.D, T0, T1, A.bwin);
+        sync_warp_loop(myflag, below, belowT1, A.D, T0, T1, A.bwin, A.trace ? A.trace + 4 * (size_t)s_ticket : nullptr);
         ss = 0.0;
     } else {
     if (y) start = A.rows[row_id(n, z, y)].start;
@@ -421,7 +439,7 @@ __global__ void __launch_bounds__(NT, 2) k_batch_bwd(PlanDev P, BatchArgs A)
     double wn_hi = 0, wts_hi = 0, wtc_hi = 0, wprev = 0;
     double c_wn = 0, c_wts = 0, c_wtc = 0, c_wf = 0, c_u = 0;
     if (warp == BW) {
-        sync_warp_loop(myflag, above, aboveEnd, A.D, tb0, tb1, A.bwin);
+        sync_warp_loop(myflag, above, aboveEnd, A.D, tb0, tb1, A.bwin, A.trace ? A.trace + 4 * (size_t)s_ticket : nullptr);
         return;
     }
     if (y) bstart = A.Tmax - (A.rows[row_id(n, z, y)].start + (n - 1 - z - y) - 1);

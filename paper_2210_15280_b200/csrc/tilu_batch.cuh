@@ -34,6 +34,8 @@ struct BatchArgs {
     int *flags;    // [G][n-3] progress counters (-1 = nothing done)
     int *ticket;   // CTA ticket counter (starts at -1)
     double *part;  // [G][n-3][32] residual partial sums or nullptr
+    unsigned long long *trace;  // debug: per CTA [ticket][4] globaltimer stamps (start, first window open,
+                                //        end, windows) or nullptr
     double arow[15];  // constant stencil (kernel-parameter constant bank: DMUL operands, no registers)
 };
 
