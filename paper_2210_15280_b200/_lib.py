@@ -89,7 +89,7 @@ def lib():
         getattr(L, name).restype = _I
     L.tilu_sweep_packed.argtypes = [_P, _P, _P, _P, _I, _I, _P, _P]
     L.tilu_sweep_packed.restype = _I
-    L.tilu_batch_schedule.argtypes = [_I, _I, _P, _P, _P, _P, _P]
+    L.tilu_batch_schedule.argtypes = [_I, _I, _I, _P, _P, _P, _P, _P]
     L.tilu_batch_schedule.restype = _I
     L.tilu_profile_enable.argtypes = [_I]
     L.tilu_profile_enable.restype = None
@@ -128,7 +128,7 @@ def profile_read() -> dict:
     return out
 
 
-def batch_schedule(level: int, bwin: int = 8) -> dict:
+def batch_schedule(level: int, bwin: int = 4, pf: int = 3) -> dict:
     """The batched path's greedy schedule as computed by libtilu (host only): per row
     (row_id order) forward start step and warp, per layer last step, D, Tmax."""
     import numpy as np
@@ -137,8 +137,8 @@ def batch_schedule(level: int, bwin: int = 8) -> dict:
     start, warp = np.zeros(max(nrows, 1), np.int32), np.zeros(max(nrows, 1), np.int32)
     T1 = np.zeros(max(n - 3, 1), np.int32)
     D, Tmax = ctypes.c_int(), ctypes.c_int()
-    k = lib().tilu_batch_schedule(level, bwin, start.ctypes.data, warp.ctypes.data, T1.ctypes.data, ctypes.byref(D),
+    k = lib().tilu_batch_schedule(level, bwin, pf, start.ctypes.data, warp.ctypes.data, T1.ctypes.data, ctypes.byref(D),
                                   ctypes.byref(Tmax))
     if k < 0:
         check(-k)
-    return {"start": start[:k], "warp": warp[:k], "T1": T1[:n - 3], "D": D.value, "Tmax": Tmax.value, "bwin": bwin}
+    return {"start": start[:k], "warp": warp[:k], "T1": T1[:n - 3], "D": D.value, "Tmax": Tmax.value, "bwin": bwin, "pf": pf}

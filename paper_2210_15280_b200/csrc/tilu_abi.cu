@@ -172,7 +172,6 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
     A.rows = static_cast<const RowSched *>(p->brows);
     A.Tmax = p->bTmax;
     A.D = p->bD;
-    A.bwin = p->bwin;
     std::memcpy(A.arow, p->harow, sizeof(A.arow));
     for (int k = 0; k < sweeps; ++k) {
         cudaMemsetAsync(sync, 0xFF, nsync * sizeof(int), s);
@@ -399,10 +398,7 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
         std::vector<LayerSched> sch;
         std::vector<RowSched> rsch;
         int T = 0, D = 0;
-        const char *ev = std::getenv("TILU_BWIN");
-        const int bwin = ev ? std::max(1, std::min(64, std::atoi(ev))) : BWIN_DEFAULT;
-        batch_schedule(n, bwin, sch, rsch, T, D);
-        p->bwin = bwin;
+        batch_schedule(n, BWIN, PF, sch, rsch, T, D);
         LayerSched *dsch = nullptr;
         RowSched *drs = nullptr;
         if ((rc = dev_upload(p, &dsch, sch.data(), sch.size())) || (rc = dev_upload(p, &drs, rsch.data(), rsch.size()))) {
@@ -547,14 +543,14 @@ static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int nt
     return check_cuda("sweep");
 }
 
-int tilu_batch_schedule(int level, int bwin, int *row_start, int *row_warp, int *layer_T1, int *D, int *Tmax)
+int tilu_batch_schedule(int level, int bwin, int pf, int *row_start, int *row_warp, int *layer_T1, int *D, int *Tmax)
 {
     if (level < 2 || level > 10) return -fail(TILU_EINVAL, "level %d outside 2..10", level);
-    if (bwin < 1 || bwin > 64) return -fail(TILU_EINVAL, "window %d outside 1..64", bwin);
+    if (bwin < 1 || bwin > 64 || pf < 0 || pf > 16) return -fail(TILU_EINVAL, "window / prefetch out of range");
     const int n = 1 << level;
     std::vector<LayerSched> sch;
     std::vector<RowSched> rs;
-    batch_schedule(n, bwin, sch, rs, *Tmax, *D);
+    batch_schedule(n, bwin, pf, sch, rs, *Tmax, *D);
     for (int z = 1; z <= n - 3; ++z) {
         layer_T1[z - 1] = sch[z - 1].T1;
         for (int wi = 0; wi < BW; ++wi)

@@ -75,23 +75,25 @@ __device__ __forceinline__ unsigned long long gtimer()
 }
 
 __device__ __forceinline__ void sync_warp_loop(int *myflag, const int *dep, int depEnd, int D, int t0, int t1,
-                                               int bwin, unsigned long long *trace)
+                                               unsigned long long *trace)
 {
+    // everything a window starting at tau0 reads from the neighbouring layer (including the PF-ahead
+    // prefetches) has step <= tau0 + BWIN + PF - 2 - D; the neighbour never publishes past depEnd
     const bool leader = (threadIdx.x & 31) == 0;
     unsigned long long waited = 0;
     if (trace && leader) trace[0] = gtimer();
-    if (leader && dep) wait_progress(dep, min(t0 + bwin - 1 - D, depEnd));
+    if (leader && dep) wait_progress(dep, min(t0 + BWIN + PF - 2 - D, depEnd));
     if (trace && leader) trace[1] = gtimer();
     __syncthreads();  // opens the first window
-    for (int tau0 = t0; tau0 <= t1; tau0 += bwin) {
-        const int tau1 = min(tau0 + bwin, t1 + 1);
+    for (int tau0 = t0; tau0 <= t1; tau0 += BWIN) {
+        const int tau1 = tau0 + BWIN;
         if (leader && dep && tau1 <= t1) {
             const unsigned long long a = trace ? gtimer() : 0;
-            wait_progress(dep, min(tau1 + bwin - 1 - D, depEnd));
+            wait_progress(dep, min(tau1 + BWIN + PF - 2 - D, depEnd));
             if (trace) waited += gtimer() - a;
         }
         __syncthreads();  // closes this window / opens the next
-        if (leader) st_release(myflag, tau1 - 1);  // MEMBAR.GPU + store: cumulative over the barrier
+        if (leader) st_release(myflag, min(tau1, t1 + 1) - 1);  // MEMBAR.GPU + store, cumulative over the barrier
     }
     if (trace && leader) {
         trace[2] = gtimer();
@@ -119,11 +121,12 @@ __device__ __forceinline__ double lq_b(const PlanDev &P, int m, int qx, int qy, 
 // ----------------------------------------------------------------------------------------------
 // host: greedy list schedule
 // ----------------------------------------------------------------------------------------------
-void batch_schedule(int n, int bwin, std::vector<LayerSched> &layers, std::vector<RowSched> &rows, int &Tmax, int &D)
+void batch_schedule(int n, int bwin, int pf, std::vector<LayerSched> &layers, std::vector<RowSched> &rows, int &Tmax,
+                    int &D)
 {
     const int nl = n - 3;
-    const int amin = bwin + 2;
-    D = 2 * bwin + 2;
+    const int amin = bwin + 1 + pf;
+    D = 2 * bwin + 1 + pf;
     layers.assign(nl, LayerSched{});
     rows.assign((size_t)(n - 3) * (n - 2) / 2 + 1, RowSched{0, 0, 0});
     Tmax = 0;
@@ -211,9 +214,157 @@ __device__ __forceinline__ void smem_march(double *tab, int lane)
 
 // ----------------------------------------------------------------------------------------------
 // forward: residual + L solve
+//
+// Per compute warp: one row at a time.  Loads run PF points ahead through a RING-slot register
+// ring; the window loop is unrolled RING (= BWIN) times so every ring index is a compile-time
+// constant: the point processed at step tau uses slot (tau - T0) % RING, the prefetch issued at
+// tau fills slot (tau + PF - T0) % RING.
 // ----------------------------------------------------------------------------------------------
+struct FwdSlot {
+    double ue, us, un, ubn, ubc, uts, utc, f, ws, wbn, wbc;
+};
+
+struct FwdRow {
+    int y, m, rid, start;
+    uint32_t oc, os, on, obn, obc, ots, otc;
+    // sliding windows: the values of point x-1 / x that point x+1 reuses
+    double u_wm, u_c, us0, un_m, ubn_m, ubc0, uts0, utc_m, ws0, wbn_m, wbc0, wprev;
+    FwdSlot ring[RING];
+    double ss;
+};
+
+__device__ __forceinline__ void fwd_load(FwdSlot &S, const double *__restrict__ u, const double *__restrict__ f,
+                                         const double *__restrict__ w, const FwdRow &R, int p)
+{
+    const uint32_t X = (uint32_t)p * 32u;
+    S.ue = u[R.oc + X + 32];
+    S.us = u[R.os + X + 32];
+    S.un = u[R.on + X];
+    S.ubn = u[R.obn + X];
+    S.ubc = u[R.obc + X + 32];
+    S.uts = u[R.ots + X + 32];
+    S.utc = u[R.otc + X];
+    S.f = f[R.oc + X];
+    S.ws = ldcg(w + R.os + X + 32);
+    S.wbn = ldcg(w + R.obn + X);
+    S.wbc = ldcg(w + R.obc + X + 32);
+}
+
+template <int K, bool EXACT, bool CONST_ROW, int SLOT>
+__device__ __forceinline__ void fwd_step(FwdRow &R, const PlanDev &P, const BatchArgs &A, int n, int z, int tau,
+                                         const double *__restrict__ u, const double *__restrict__ f,
+                                         double *__restrict__ w, double *tab, int lane)
+{
+    if (!R.y) return;
+    const int x = tau - R.start + 1;
+    if (x < 1) return;
+    if (x == 1) {  // row start: offsets, seed table, windows, ring fill for points 1..PF
+        const int y = R.y;
+        R.m = n - 1 - z - y;
+        R.rid = row_id(n, z, y);
+        R.oc = (uint32_t)row_offset(n, z, y) * 32u;
+        R.os = (uint32_t)row_offset(n, z, y - 1) * 32u;
+        R.on = (uint32_t)row_offset(n, z, y + 1) * 32u;
+        R.obn = (uint32_t)row_offset(n, z - 1, y + 1) * 32u;
+        R.obc = (uint32_t)row_offset(n, z - 1, y) * 32u;
+        R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
+        R.otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
+        smem_load_table<7, K>(tab, P.seedF + (int64_t)R.rid * 7 * K, lane);
+        R.u_wm = u[R.oc];
+        R.u_c = u[R.oc + 32];
+        R.us0 = u[R.os + 32];
+        R.un_m = u[R.on];
+        R.ubn_m = u[R.obn];
+        R.ubc0 = u[R.obc + 32];
+        R.uts0 = u[R.ots + 32];
+        R.utc_m = u[R.otc];
+        R.ws0 = ldcg(w + R.os + 32);
+        R.wbn_m = ldcg(w + R.obn);
+        R.wbc0 = ldcg(w + R.obc + 32);
+        R.wprev = 0.0;
+#pragma unroll
+        for (int q = 0; q < PF; ++q)
+            if (1 + q <= R.m) fwd_load(R.ring[(SLOT + q) % RING], u, f, w, R, 1 + q);
+    }
+    if (x + PF <= R.m) fwd_load(R.ring[(SLOT + PF) % RING], u, f, w, R, x + PF);
+    const FwdSlot &C = R.ring[SLOT];
+    double ap[15];
+    const double *a = A.arow;
+    if (!CONST_ROW) {
+        const double *ar = P.arows + 15 * (int64_t)(R.oc / 32u + x);
+#pragma unroll
+        for (int i = 0; i < 15; ++i) ap[i] = ar[i];
+        a = ap;
+    }
+    // residual in stencil_apply order (_kernels.py:255-266), then f - A u
+    double acc = EXACT ? dmul(a[7], R.u_c) : a[7] * R.u_c;
+    acc = madd<EXACT>(acc, a[0], R.u_wm);
+    acc = madd<EXACT>(acc, a[1], R.us0);
+    acc = madd<EXACT>(acc, a[2], C.us);
+    acc = madd<EXACT>(acc, a[3], R.ubn_m);
+    acc = madd<EXACT>(acc, a[4], C.ubn);
+    acc = madd<EXACT>(acc, a[5], R.ubc0);
+    acc = madd<EXACT>(acc, a[6], C.ubc);
+    acc = madd<EXACT>(acc, a[8], C.ue);
+    acc = madd<EXACT>(acc, a[9], C.un);
+    acc = madd<EXACT>(acc, a[10], R.un_m);
+    acc = madd<EXACT>(acc, a[11], C.uts);
+    acc = madd<EXACT>(acc, a[12], R.uts0);
+    acc = madd<EXACT>(acc, a[13], C.utc);
+    acc = madd<EXACT>(acc, a[14], R.utc_m);
+    const double r = dsub(C.f, acc);
+    R.ss = fma(r, r, R.ss);
+    // L entries: NDDF marchers (shared table) or the V1 band store
+    double L[7];
+    const int y = R.y;
+    if (P.variant == 1 && in_band_b(x, y, z, R.m)) {
+        const double *st = P.store + 9 * (int64_t)band_idx_b(P, R.rid, x, y, z);
+#pragma unroll
+        for (int mm = 0; mm < 7; ++mm) L[mm] = st[mm];
+    } else {
+#pragma unroll
+        for (int mm = 0; mm < 7; ++mm) L[mm] = tab[mm * K];
+    }
+    double v;
+    if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
+        v = msub<true>(r, L[0], R.wprev);
+        v = msub<true>(v, L[1], R.ws0);
+        v = msub<true>(v, L[2], C.ws);
+        v = msub<true>(v, L[3], R.wbn_m);
+        v = msub<true>(v, L[4], C.wbn);
+        v = msub<true>(v, L[5], R.wbc0);
+        v = msub<true>(v, L[6], C.wbc);
+    } else {  // own-row term last: one FMA on the row's dependency chain
+        v = msub<false>(r, L[1], R.ws0);
+        v = msub<false>(v, L[2], C.ws);
+        v = msub<false>(v, L[3], R.wbn_m);
+        v = msub<false>(v, L[4], C.wbn);
+        v = msub<false>(v, L[5], R.wbc0);
+        v = msub<false>(v, L[6], C.wbc);
+        v = msub<false>(v, L[0], R.wprev);
+    }
+    w[R.oc + (uint32_t)x * 32u] = v;
+    smem_march<7, K>(tab, lane);
+    R.u_wm = R.u_c;
+    R.u_c = C.ue;
+    R.us0 = C.us;
+    R.un_m = C.un;
+    R.ubn_m = C.ubn;
+    R.ubc0 = C.ubc;
+    R.uts0 = C.uts;
+    R.utc_m = C.utc;
+    R.ws0 = C.ws;
+    R.wbn_m = C.wbn;
+    R.wbc0 = C.wbc;
+    R.wprev = v;
+    if (x == R.m) {
+        R.y = A.rows[R.rid].next;
+        if (R.y) R.start = A.rows[row_id(n, z, R.y)].start;
+    }
+}
+
 template <int K, bool EXACT, bool CONST_ROW>
-__global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
 {
     __shared__ int s_ticket;
     __shared__ double s_red[BW][32];
@@ -223,182 +374,33 @@ __global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
     __syncthreads();
     const int nl = P.n - 3;
     const int zi = s_ticket / A.G, g = s_ticket - (s_ticket / A.G) * A.G;
-    double *tab = s_tab[warp < BW ? warp : 0];
     const int n = P.n, z = zi + 1;
     const int T0 = A.sched[zi].T0, T1 = A.sched[zi].T1;
-    const size_t gb = (size_t)g * P.grid * 32 + lane;
-    const double *__restrict__ u = A.u + gb;
-    const double *__restrict__ f = A.f + gb;
-    double *__restrict__ w = A.w + gb;
     int *myflag = A.flags + g * nl + zi;
-    const int *below = z > 1 ? myflag - 1 : nullptr;
-    const int belowT1 = z > 1 ? A.sched[zi - 1].T1 : 0;
-
-    double ap[15];  // per-point stencil rows (non-constant operators)
-    const double *a = CONST_ROW ? A.arow : ap;
-
-    int y = A.sched[zi].first[warp];
-    int m = 0, rid = 0, start = 0;
-    uint32_t oc = 0, os = 0, on = 0, obn = 0, obc = 0, ots = 0, otc = 0;
-    // sliding windows: values of point x-1 / x that point x+1 reuses
-    double u_wm = 0, u_c = 0, us0 = 0, un_m = 0, ubn_m = 0, ubc0 = 0, uts0 = 0, utc_m = 0;
-    double ws0 = 0, wbn_m = 0, wbc0 = 0, wprev = 0;
-    // newest entries of the current point (prefetched while the previous point computed)
-    double c_ue = 0, c_us = 0, c_un = 0, c_ubn = 0, c_ubc = 0, c_uts = 0, c_utc = 0, c_f = 0;
-    double c_ws = 0, c_wbn = 0, c_wbc = 0;
-    double ss = 0.0;
     if (warp == BW) {
-        sync_warp_loop(myflag, below, belowT1, A.D, T0, T1, A.bwin, A.trace ? A.trace + 4 * (size_t)s_ticket : nullptr);
-        ss = 0.0;
+        sync_warp_loop(myflag, z > 1 ? myflag - 1 : nullptr, z > 1 ? A.sched[zi - 1].T1 : 0, A.D, T0, T1,
+                       A.trace ? A.trace + 4 * (size_t)s_ticket : nullptr);
     } else {
-    if (y) start = A.rows[row_id(n, z, y)].start;
-    __syncthreads();  // first window opened by the sync warp
-    for (int tau0 = T0; tau0 <= T1; tau0 += A.bwin) {
-        const int tau1 = min(tau0 + A.bwin, T1 + 1);
-        for (int tau = tau0; tau < tau1; ++tau) {
-            if (!y) break;
-            const int x = tau - start + 1;
-            if (x < 1) continue;
-            if (x == 1) {  // row start: offsets, seed table, stencil windows, point-1 values
-                m = n - 1 - z - y;
-                rid = row_id(n, z, y);
-                oc = (uint32_t)row_offset(n, z, y) * 32u;
-                os = (uint32_t)row_offset(n, z, y - 1) * 32u;
-                on = (uint32_t)row_offset(n, z, y + 1) * 32u;
-                obn = (uint32_t)row_offset(n, z - 1, y + 1) * 32u;
-                obc = (uint32_t)row_offset(n, z - 1, y) * 32u;
-                ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
-                otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
-                smem_load_table<7, K>(tab, P.seedF + (int64_t)rid * 7 * K, lane);
-                u_wm = u[oc];
-                u_c = u[oc + 32];
-                us0 = u[os + 32];
-                un_m = u[on];
-                ubn_m = u[obn];
-                ubc0 = u[obc + 32];
-                uts0 = u[ots + 32];
-                utc_m = u[otc];
-                ws0 = ldcg(w + os + 32);
-                wbn_m = ldcg(w + obn);
-                wbc0 = ldcg(w + obc + 32);
-                wprev = 0.0;
-                c_ue = u[oc + 64];
-                c_us = u[os + 64];
-                c_un = u[on + 32];
-                c_ubn = u[obn + 32];
-                c_ubc = u[obc + 64];
-                c_uts = u[ots + 64];
-                c_utc = u[otc + 32];
-                c_f = f[oc + 32];
-                c_ws = ldcg(w + os + 64);
-                c_wbn = ldcg(w + obn + 32);
-                c_wbc = ldcg(w + obc + 64);
-            }
-            const uint32_t X = (uint32_t)x * 32u;
-            // prefetch point x+1 (safe: AMIN and the window's progress wait cover it)
-            double n_ue = 0, n_us = 0, n_un = 0, n_ubn = 0, n_ubc = 0, n_uts = 0, n_utc = 0, n_f = 0;
-            double n_ws = 0, n_wbn = 0, n_wbc = 0;
-            if (x < m) {
-                const uint32_t X1 = X + 32u;
-                n_ue = u[oc + X1 + 32];
-                n_us = u[os + X1 + 32];
-                n_un = u[on + X1];
-                n_ubn = u[obn + X1];
-                n_ubc = u[obc + X1 + 32];
-                n_uts = u[ots + X1 + 32];
-                n_utc = u[otc + X1];
-                n_f = f[oc + X1];
-                n_ws = ldcg(w + os + X1 + 32);
-                n_wbn = ldcg(w + obn + X1);
-                n_wbc = ldcg(w + obc + X1 + 32);
-            }
-            if (!CONST_ROW) {
-                const double *ar = P.arows + 15 * (int64_t)(oc / 32u + x);
-#pragma unroll
-                for (int i = 0; i < 15; ++i) ap[i] = ar[i];
-            }
-            // residual in stencil_apply order (_kernels.py:255-266), then f - A u
-            double acc = EXACT ? dmul(a[7], u_c) : a[7] * u_c;
-            acc = madd<EXACT>(acc, a[0], u_wm);
-            acc = madd<EXACT>(acc, a[1], us0);
-            acc = madd<EXACT>(acc, a[2], c_us);
-            acc = madd<EXACT>(acc, a[3], ubn_m);
-            acc = madd<EXACT>(acc, a[4], c_ubn);
-            acc = madd<EXACT>(acc, a[5], ubc0);
-            acc = madd<EXACT>(acc, a[6], c_ubc);
-            acc = madd<EXACT>(acc, a[8], c_ue);
-            acc = madd<EXACT>(acc, a[9], c_un);
-            acc = madd<EXACT>(acc, a[10], un_m);
-            acc = madd<EXACT>(acc, a[11], c_uts);
-            acc = madd<EXACT>(acc, a[12], uts0);
-            acc = madd<EXACT>(acc, a[13], c_utc);
-            acc = madd<EXACT>(acc, a[14], utc_m);
-            const double r = dsub(c_f, acc);
-            ss = fma(r, r, ss);
-            // L entries: NDDF marchers or the V1 band store
-            double L[7];
-            if (P.variant == 1 && in_band_b(x, y, z, m)) {
-                const double *st = P.store + 9 * (int64_t)band_idx_b(P, rid, x, y, z);
-#pragma unroll
-                for (int mm = 0; mm < 7; ++mm) L[mm] = st[mm];
-            } else {
-#pragma unroll
-                for (int mm = 0; mm < 7; ++mm) L[mm] = tab[mm * K];
-            }
-            double v;
-            if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
-                v = msub<true>(r, L[0], wprev);
-                v = msub<true>(v, L[1], ws0);
-                v = msub<true>(v, L[2], c_ws);
-                v = msub<true>(v, L[3], wbn_m);
-                v = msub<true>(v, L[4], c_wbn);
-                v = msub<true>(v, L[5], wbc0);
-                v = msub<true>(v, L[6], c_wbc);
-            } else {      // own-row term last: one FMA on the row's dependency chain
-                v = msub<false>(r, L[1], ws0);
-                v = msub<false>(v, L[2], c_ws);
-                v = msub<false>(v, L[3], wbn_m);
-                v = msub<false>(v, L[4], c_wbn);
-                v = msub<false>(v, L[5], wbc0);
-                v = msub<false>(v, L[6], c_wbc);
-                v = msub<false>(v, L[0], wprev);
-            }
-            w[oc + X] = v;
-            smem_march<7, K>(tab, lane);
-            // slide the windows
-            u_wm = u_c;
-            u_c = c_ue;
-            us0 = c_us;
-            un_m = c_un;
-            ubn_m = c_ubn;
-            ubc0 = c_ubc;
-            uts0 = c_uts;
-            utc_m = c_utc;
-            ws0 = c_ws;
-            wbn_m = c_wbn;
-            wbc0 = c_wbc;
-            wprev = v;
-            c_ue = n_ue;
-            c_us = n_us;
-            c_un = n_un;
-            c_ubn = n_ubn;
-            c_ubc = n_ubc;
-            c_uts = n_uts;
-            c_utc = n_utc;
-            c_f = n_f;
-            c_ws = n_ws;
-            c_wbn = n_wbn;
-            c_wbc = n_wbc;
-            if (x == m) {
-                y = A.rows[rid].next;
-                if (y) start = A.rows[row_id(n, z, y)].start;
-            }
+        const size_t gb = (size_t)g * P.grid * 32 + lane;
+        const double *__restrict__ u = A.u + gb;
+        const double *__restrict__ f = A.f + gb;
+        double *__restrict__ w = A.w + gb;
+        double *tab = s_tab[warp];
+        FwdRow R;
+        R.y = A.sched[zi].first[warp];
+        R.start = R.y ? A.rows[row_id(n, z, R.y)].start : 0;
+        R.ss = 0.0;
+        __syncthreads();  // first window opened by the sync warp
+        for (int tau0 = T0; tau0 <= T1; tau0 += BWIN) {
+            fwd_step<K, EXACT, CONST_ROW, 0>(R, P, A, n, z, tau0 + 0, u, f, w, tab, lane);
+            fwd_step<K, EXACT, CONST_ROW, 1>(R, P, A, n, z, tau0 + 1, u, f, w, tab, lane);
+            fwd_step<K, EXACT, CONST_ROW, 2>(R, P, A, n, z, tau0 + 2, u, f, w, tab, lane);
+            fwd_step<K, EXACT, CONST_ROW, 3>(R, P, A, n, z, tau0 + 3, u, f, w, tab, lane);
+            __syncthreads();
         }
-        __syncthreads();
-    }
+        s_red[warp][lane] = R.ss;
     }
     if (A.part) {
-        if (warp < BW) s_red[warp][lane] = ss;
         __syncthreads();
         if (warp == 0) {
             double t = 0.0;
@@ -412,119 +414,130 @@ __global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
 // ----------------------------------------------------------------------------------------------
 // backward: D^{-1} + L^T solve + update, exact time reversal of the forward schedule
 // ----------------------------------------------------------------------------------------------
+struct BwdSlot {
+    double wn, wts, wtc, wf, u;
+};
+
+struct BwdRow {
+    int y, m, rid, bstart;  // bstart: backward step of the row's first point (x = m)
+    uint32_t oc, on, ots, otc;
+    double wn_hi, wts_hi, wtc_hi, wprev;
+    BwdSlot ring[RING];
+};
+
+__device__ __forceinline__ void bwd_load(BwdSlot &S, const double *__restrict__ u, const double *__restrict__ w,
+                                         const BwdRow &R, int x)
+{
+    const uint32_t X = (uint32_t)x * 32u;
+    S.wn = ldcg(w + R.on + X - 32);
+    S.wts = ldcg(w + R.ots + X);
+    S.wtc = ldcg(w + R.otc + X - 32);
+    S.wf = w[R.oc + X];
+    S.u = u[R.oc + X];
+}
+
+template <int K, bool EXACT, int SLOT>
+__device__ __forceinline__ void bwd_step(BwdRow &R, const PlanDev &P, const BatchArgs &A, int n, int z, int tau,
+                                         double *__restrict__ u, double *__restrict__ w, double *tab, int lane)
+{
+    if (!R.y) return;
+    const int k = tau - R.bstart;  // 0-based position along the descending row
+    if (k < 0) return;
+    const int y = R.y;
+    if (k == 0) {
+        R.m = n - 1 - z - y;
+        R.rid = row_id(n, z, y);
+        R.oc = (uint32_t)row_offset(n, z, y) * 32u;
+        R.on = (uint32_t)row_offset(n, z, y + 1) * 32u;
+        R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
+        R.otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
+        smem_load_table<8, K>(tab, P.seedB + (int64_t)R.rid * 8 * K, lane);
+        const uint32_t M = (uint32_t)R.m * 32u;
+        R.wn_hi = ldcg(w + R.on + M);
+        R.wts_hi = ldcg(w + R.ots + M + 32);
+        R.wtc_hi = ldcg(w + R.otc + M);
+        R.wprev = 0.0;
+#pragma unroll
+        for (int q = 0; q < PF; ++q)
+            if (R.m - q >= 1) bwd_load(R.ring[(SLOT + q) % RING], u, w, R, R.m - q);
+    }
+    const int x = R.m - k;
+    if (x - PF >= 1) bwd_load(R.ring[(SLOT + PF) % RING], u, w, R, x - PF);
+    const BwdSlot &C = R.ring[SLOT];
+    const bool band = P.variant == 1 && in_band_b(x, y, z, R.m);
+    const double inv_d = band ? P.store[9 * (int64_t)band_idx_b(P, R.rid, x, y, z) + 8] : tab[7 * K];
+    double Lq[7];
+    Lq[0] = lq_b(P, 0, x + 1, y, z, tab[0 * K]);
+    Lq[1] = lq_b(P, 1, x, y + 1, z, tab[1 * K]);
+    Lq[2] = lq_b(P, 2, x - 1, y + 1, z, tab[2 * K]);
+    Lq[3] = lq_b(P, 3, x + 1, y - 1, z + 1, tab[3 * K]);
+    Lq[4] = lq_b(P, 4, x, y - 1, z + 1, tab[4 * K]);
+    Lq[5] = lq_b(P, 5, x, y, z + 1, tab[5 * K]);
+    Lq[6] = lq_b(P, 6, x - 1, y, z + 1, tab[6 * K]);
+    double v = EXACT ? dmul(inv_d, C.wf) : inv_d * C.wf;
+    if (EXACT) {  // reference order (_kernels.py:404-425)
+        v = msub<true>(v, Lq[0], R.wprev);
+        v = msub<true>(v, Lq[1], R.wn_hi);
+        v = msub<true>(v, Lq[2], C.wn);
+        v = msub<true>(v, Lq[3], R.wts_hi);
+        v = msub<true>(v, Lq[4], C.wts);
+        v = msub<true>(v, Lq[5], R.wtc_hi);
+        v = msub<true>(v, Lq[6], C.wtc);
+    } else {
+        v = msub<false>(v, Lq[1], R.wn_hi);
+        v = msub<false>(v, Lq[2], C.wn);
+        v = msub<false>(v, Lq[3], R.wts_hi);
+        v = msub<false>(v, Lq[4], C.wts);
+        v = msub<false>(v, Lq[5], R.wtc_hi);
+        v = msub<false>(v, Lq[6], C.wtc);
+        v = msub<false>(v, Lq[0], R.wprev);
+    }
+    const uint32_t X = (uint32_t)x * 32u;
+    w[R.oc + X] = v;
+    u[R.oc + X] = dadd(C.u, v);
+    smem_march<8, K>(tab, lane);
+    R.wn_hi = C.wn;
+    R.wts_hi = C.wts;
+    R.wtc_hi = C.wtc;
+    R.wprev = v;
+    if (x == 1) {
+        R.y = A.rows[R.rid].prev;
+        if (R.y) R.bstart = A.Tmax - (A.rows[row_id(n, z, R.y)].start + (n - 1 - z - R.y) - 1);
+    }
+}
+
 template <int K, bool EXACT>
-__global__ void __launch_bounds__(NT, 2) k_batch_bwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
 {
     __shared__ int s_ticket;
     __shared__ double s_tab[BW][8 * K];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_ticket = atomicAdd(A.ticket, 1) + 1;
     __syncthreads();
-    double *tab = s_tab[warp < BW ? warp : 0];
     const int nl = P.n - 3;
     const int li = s_ticket / A.G, g = s_ticket - li * A.G;
     const int zi = nl - 1 - li;
     const int n = P.n, z = zi + 1;
+    int *myflag = A.flags + g * nl + zi;
+    const int tb0 = A.Tmax - A.sched[zi].T1, tb1 = A.Tmax - A.sched[zi].T0;
+    if (warp == BW) {
+        sync_warp_loop(myflag, z < nl ? myflag + 1 : nullptr, z < nl ? A.Tmax - A.sched[zi + 1].T0 : 0, A.D, tb0,
+                       tb1, A.trace ? A.trace + 4 * (size_t)s_ticket : nullptr);
+        return;
+    }
     const size_t gb = (size_t)g * P.grid * 32 + lane;
     double *__restrict__ u = A.u + gb;
     double *__restrict__ w = A.w + gb;
-    int *myflag = A.flags + g * nl + zi;
-    const int *above = z < nl ? myflag + 1 : nullptr;
-    const int aboveEnd = z < nl ? A.Tmax - A.sched[zi + 1].T0 : 0;
-    const int tb0 = A.Tmax - A.sched[zi].T1, tb1 = A.Tmax - A.sched[zi].T0;
-
-    int y = A.sched[zi].last[warp];
-    int m = 0, rid = 0, bstart = 0;  // bstart: backward step of the row's first point (x = m)
-    uint32_t oc = 0, on = 0, ots = 0, otc = 0;
-    double wn_hi = 0, wts_hi = 0, wtc_hi = 0, wprev = 0;
-    double c_wn = 0, c_wts = 0, c_wtc = 0, c_wf = 0, c_u = 0;
-    if (warp == BW) {
-        sync_warp_loop(myflag, above, aboveEnd, A.D, tb0, tb1, A.bwin, A.trace ? A.trace + 4 * (size_t)s_ticket : nullptr);
-        return;
-    }
-    if (y) bstart = A.Tmax - (A.rows[row_id(n, z, y)].start + (n - 1 - z - y) - 1);
+    double *tab = s_tab[warp];
+    BwdRow R;
+    R.y = A.sched[zi].last[warp];
+    R.bstart = R.y ? A.Tmax - (A.rows[row_id(n, z, R.y)].start + (n - 1 - z - R.y) - 1) : 0;
     __syncthreads();  // first window opened by the sync warp
-    for (int tau0 = tb0; tau0 <= tb1; tau0 += A.bwin) {
-        const int tau1 = min(tau0 + A.bwin, tb1 + 1);
-        for (int tau = tau0; tau < tau1; ++tau) {
-            if (!y) break;
-            const int k = tau - bstart;  // 0-based position along the descending row
-            if (k < 0) continue;
-            if (k == 0) {  // row start at x = m
-                m = n - 1 - z - y;
-                rid = row_id(n, z, y);
-                oc = (uint32_t)row_offset(n, z, y) * 32u;
-                on = (uint32_t)row_offset(n, z, y + 1) * 32u;
-                ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
-                otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
-                smem_load_table<8, K>(tab, P.seedB + (int64_t)rid * 8 * K, lane);
-                const uint32_t M = (uint32_t)m * 32u;
-                wn_hi = ldcg(w + on + M);
-                wts_hi = ldcg(w + ots + M + 32);
-                wtc_hi = ldcg(w + otc + M);
-                wprev = 0.0;
-                c_wn = ldcg(w + on + M - 32);
-                c_wts = ldcg(w + ots + M);
-                c_wtc = ldcg(w + otc + M - 32);
-                c_wf = w[oc + M];
-                c_u = u[oc + M];
-            }
-            const int x = m - k;
-            const uint32_t X = (uint32_t)x * 32u;
-            double n_wn = 0, n_wts = 0, n_wtc = 0, n_wf = 0, n_u = 0;
-            if (x > 1) {
-                const uint32_t X1 = X - 32u;
-                n_wn = ldcg(w + on + X1 - 32);
-                n_wts = ldcg(w + ots + X1);
-                n_wtc = ldcg(w + otc + X1 - 32);
-                n_wf = w[oc + X1];
-                n_u = u[oc + X1];
-            }
-            const bool band = P.variant == 1 && in_band_b(x, y, z, m);
-            const double inv_d = band ? P.store[9 * (int64_t)band_idx_b(P, rid, x, y, z) + 8] : tab[7 * K];
-            double Lq[7];
-            Lq[0] = lq_b(P, 0, x + 1, y, z, tab[0 * K]);
-            Lq[1] = lq_b(P, 1, x, y + 1, z, tab[1 * K]);
-            Lq[2] = lq_b(P, 2, x - 1, y + 1, z, tab[2 * K]);
-            Lq[3] = lq_b(P, 3, x + 1, y - 1, z + 1, tab[3 * K]);
-            Lq[4] = lq_b(P, 4, x, y - 1, z + 1, tab[4 * K]);
-            Lq[5] = lq_b(P, 5, x, y, z + 1, tab[5 * K]);
-            Lq[6] = lq_b(P, 6, x - 1, y, z + 1, tab[6 * K]);
-            double v = EXACT ? dmul(inv_d, c_wf) : inv_d * c_wf;
-            if (EXACT) {  // reference order (_kernels.py:404-425)
-                v = msub<true>(v, Lq[0], wprev);
-                v = msub<true>(v, Lq[1], wn_hi);
-                v = msub<true>(v, Lq[2], c_wn);
-                v = msub<true>(v, Lq[3], wts_hi);
-                v = msub<true>(v, Lq[4], c_wts);
-                v = msub<true>(v, Lq[5], wtc_hi);
-                v = msub<true>(v, Lq[6], c_wtc);
-            } else {
-                v = msub<false>(v, Lq[1], wn_hi);
-                v = msub<false>(v, Lq[2], c_wn);
-                v = msub<false>(v, Lq[3], wts_hi);
-                v = msub<false>(v, Lq[4], c_wts);
-                v = msub<false>(v, Lq[5], wtc_hi);
-                v = msub<false>(v, Lq[6], c_wtc);
-                v = msub<false>(v, Lq[0], wprev);
-            }
-            w[oc + X] = v;
-            u[oc + X] = dadd(c_u, v);
-            smem_march<8, K>(tab, lane);
-            wn_hi = c_wn;
-            wts_hi = c_wts;
-            wtc_hi = c_wtc;
-            wprev = v;
-            c_wn = n_wn;
-            c_wts = n_wts;
-            c_wtc = n_wtc;
-            c_wf = n_wf;
-            c_u = n_u;
-            if (x == 1) {
-                y = A.rows[rid].prev;
-                if (y) bstart = A.Tmax - (A.rows[row_id(n, z, y)].start + (n - 1 - z - y) - 1);
-            }
-        }
+    for (int tau0 = tb0; tau0 <= tb1; tau0 += BWIN) {
+        bwd_step<K, EXACT, 0>(R, P, A, n, z, tau0 + 0, u, w, tab, lane);
+        bwd_step<K, EXACT, 1>(R, P, A, n, z, tau0 + 1, u, w, tab, lane);
+        bwd_step<K, EXACT, 2>(R, P, A, n, z, tau0 + 2, u, w, tab, lane);
+        bwd_step<K, EXACT, 3>(R, P, A, n, z, tau0 + 3, u, w, tab, lane);
         __syncthreads();
     }
 }

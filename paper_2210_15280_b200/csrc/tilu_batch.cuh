@@ -8,8 +8,11 @@ namespace tilu {
 
 constexpr int BW = 8;        // compute warps per CTA = rows of one z-layer in flight
 constexpr int NT = (BW + 1) * 32;  // + one sync warp (progress wait / publish off the compute path)
-constexpr int BWIN_DEFAULT = 8;  // synchronisation window (steps between CTA barriers); TILU_BWIN overrides
-// min. start offset of consecutive rows of a layer = window + 2 (one-point prefetch)
+constexpr int BWIN = 4;      // synchronisation window (steps between CTA barriers)
+constexpr int PF = 3;        // load prefetch distance (points)
+constexpr int RING = 4;      // register ring slots (== BWIN: static slot indices in the unrolled window)
+static_assert(RING == BWIN && PF < RING, "ring layout");
+// min. start offset of consecutive rows of a layer: window + 1 + PF
 
 // Per-row schedule (indexed by row_id(n, z, y)): the forward step of point (x, y, z) is
 // start + x - 1; next / prev = the neighbouring rows (same layer) owned by the same warp, 0 = none.
@@ -30,7 +33,7 @@ struct BatchArgs {
     int G, ntets;
     const LayerSched *sched;  // [n-3]
     const RowSched *rows;     // [nrows]
-    int Tmax, D, bwin;
+    int Tmax, D;
     int *flags;    // [G][n-3] progress counters (-1 = nothing done)
     int *ticket;   // CTA ticket counter (starts at -1)
     double *part;  // [G][n-3][32] residual partial sums or nullptr
@@ -40,6 +43,7 @@ struct BatchArgs {
 };
 
 // Host: greedy list schedule of one level (tilu_batch.cu header comment).
-void batch_schedule(int n, int bwin, std::vector<LayerSched> &layers, std::vector<RowSched> &rows, int &Tmax, int &D);
+void batch_schedule(int n, int bwin, int pf, std::vector<LayerSched> &layers, std::vector<RowSched> &rows, int &Tmax,
+                    int &D);
 
 }  // namespace tilu

@@ -41,7 +41,7 @@ struct tilu_plan {
     // batched (packed) path schedule
     const void *bsched;  // device LayerSched[n-3]
     const void *brows;   // device RowSched[nrows]
-    int bTmax, bD, bwin;
+    int bTmax, bD;
     double harow[15];  // host copy of the constant stencil (batched kernel parameters)
     int flags;
     int64_t interior;

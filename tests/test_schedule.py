@@ -16,8 +16,8 @@ def row_id(n, z, y):
     return (z - 1) * (n - 2) - (z - 1) * z // 2 + (y - 1)
 
 
-def schedule(level, bwin):
-    s = _lib.batch_schedule(level, bwin)
+def schedule(level, bwin, pf=1):
+    s = _lib.batch_schedule(level, bwin, pf)
     n = 2 ** level
     T = {}
     for z in range(1, n - 2):
@@ -33,15 +33,18 @@ def window_start(t, t0, bwin):
     return t0 + ((t - t0) // bwin) * bwin
 
 
-@pytest.mark.parametrize("bwin", [1, 2, 8])
+WP = [(4, 3), (1, 1), (2, 1), (8, 1), (4, 0)]
+
+
+@pytest.mark.parametrize("bwin,pf", WP)
 @pytest.mark.parametrize("level", [2, 3, 4, 5, 6])
-def test_forward_reads_are_safe(level, bwin):
-    s, T, T0 = schedule(level, bwin)
+def test_forward_reads_are_safe(level, bwin, pf):
+    s, T, T0 = schedule(level, bwin, pf)
     n = 2 ** level
     D = s["D"]
     for (x, y, z), t in T.items():
-        # the values of point p are loaded at t (row start) or prefetched at t - 1
-        load_t = t if x == 1 else t - 1
+        # points 1..pf are loaded at the row's first step, later ones pf steps ahead
+        load_t = t - x + 1 if x <= pf else t - pf
         ws = window_start(load_t, T0[z], bwin)
         for dx, dy, dz in LOWER:
             q = (x + dx, y + dy, z + dz)
@@ -53,14 +56,14 @@ def test_forward_reads_are_safe(level, bwin):
             elif dz == 0:
                 assert tq < ws, ((x, y, z), q)          # closed window of this CTA
             else:
-                need = min(ws + bwin - 1 - D, int(s["T1"][z - 2]))
+                need = min(ws + bwin + pf - 2 - D, int(s["T1"][z - 2]))
                 assert tq <= need, ((x, y, z), q)       # covered by the progress wait
 
 
-@pytest.mark.parametrize("bwin", [2, 8])
+@pytest.mark.parametrize("bwin,pf", WP)
 @pytest.mark.parametrize("level", [3, 5, 7, 9])
-def test_warps_own_one_row_at_a_time(level, bwin):
-    s = _lib.batch_schedule(level, bwin)
+def test_warps_own_one_row_at_a_time(level, bwin, pf):
+    s = _lib.batch_schedule(level, bwin, pf)
     n = 2 ** level
     for z in range(1, n - 2):
         busy = {}
@@ -71,11 +74,11 @@ def test_warps_own_one_row_at_a_time(level, bwin):
             assert st >= busy.get(w, -1), (z, y)
             busy[w] = st + m
             if y > 1:
-                assert st >= int(s["start"][r - 1]) + bwin + 2
+                assert st >= int(s["start"][r - 1]) + bwin + 1 + pf
 
 
-def _simulate(level, backward, bwin):
-    s, _, T0 = schedule(level, bwin)
+def _simulate(level, backward, bwin, pf):
+    s, _, T0 = schedule(level, bwin, pf)
     n = 2 ** level
     nl = n - 3
     Tmax, D = s["Tmax"], s["D"]
@@ -91,7 +94,7 @@ def _simulate(level, backward, bwin):
             if z in done:
                 continue
             dep = z + 1 if backward else z - 1
-            if dep in T1 and prog[dep] < min(pos[z] + bwin - 1 - D, hi[dep]):
+            if dep in T1 and prog[dep] < min(pos[z] + bwin + pf - 2 - D, hi[dep]):
                 continue
             t1 = min(pos[z] + bwin, hi[z] + 1)
             prog[z], pos[z], moved = t1 - 1, t1, True
@@ -100,28 +103,29 @@ def _simulate(level, backward, bwin):
     return len(done) == nl
 
 
-@pytest.mark.parametrize("bwin", [1, 2, 8])
+@pytest.mark.parametrize("bwin,pf", WP)
 @pytest.mark.parametrize("level", [2, 3, 4, 5, 6, 7, 8])
-def test_handoff_completes(level, bwin):
-    assert _simulate(level, backward=False, bwin=bwin)
-    assert _simulate(level, backward=True, bwin=bwin)
+def test_handoff_completes(level, bwin, pf):
+    assert _simulate(level, backward=False, bwin=bwin, pf=pf)
+    assert _simulate(level, backward=True, bwin=bwin, pf=pf)
 
 
 UPPER_READS = [(1, 0, 0), (0, 1, 0), (-1, 1, 0), (1, -1, 1), (0, -1, 1), (0, 0, 1), (-1, 0, 1)]
 
 
-@pytest.mark.parametrize("bwin", [1, 2, 8])
+@pytest.mark.parametrize("bwin,pf", WP)
 @pytest.mark.parametrize("level", [2, 3, 4, 5, 6])
-def test_backward_reads_are_safe(level, bwin):
+def test_backward_reads_are_safe(level, bwin, pf):
     """Backward = time reversal: point p runs at Tmax - T(p) and reads its upper neighbours."""
-    s, T, T0 = schedule(level, bwin)
+    s, T, T0 = schedule(level, bwin, pf)
     n = 2 ** level
     D, Tmax = s["D"], s["Tmax"]
     T1 = {z: int(s["T1"][z - 1]) for z in range(1, n - 2)}
     for (x, y, z), t in T.items():
         tb = Tmax - t
         m = n - 1 - z - y
-        load_t = tb if x == m else tb - 1
+        k = m - x                      # 0-based position along the descending row
+        load_t = tb - k if k < pf else tb - pf
         ws = window_start(load_t, Tmax - T1[z], bwin)
         for dx, dy, dz in UPPER_READS:
             q = (x + dx, y + dy, z + dz)
@@ -133,5 +137,5 @@ def test_backward_reads_are_safe(level, bwin):
             elif dz == 0:
                 assert tq < ws, ((x, y, z), q)
             else:
-                need = min(ws + bwin - 1 - D, Tmax - T0[z + 1])
+                need = min(ws + bwin + pf - 2 - D, Tmax - T0[z + 1])
                 assert tq <= need, ((x, y, z), q)
