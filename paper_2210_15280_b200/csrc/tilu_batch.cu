@@ -226,7 +226,9 @@ struct FwdSlot {
 
 struct FwdRow {
     int y, m, rid, start;
+    int boff;           // first band-store entry of the row (V1)
     uint32_t oc, os, on, obn, obc, ots, otc;
+    double lring[RING];  // lane m < 7: prefetched band-store entry L_m of the slot's point (V1)
     // sliding windows: the values of point x-1 / x that point x+1 reuses
     double u_wm, u_c, us0, un_m, ubn_m, ubc0, uts0, utc_m, ws0, wbn_m, wbc0, wprev;
     FwdSlot ring[RING];
@@ -250,10 +252,17 @@ __device__ __forceinline__ void fwd_load(FwdSlot &S, const double *__restrict__ 
     S.wbc = ldcg(w + R.obc + X + 32);
 }
 
+// Lane m < 7 fetches the V1 band-store entry L_m of point p (uniform over the warp's tets) ahead.
+__device__ __forceinline__ void fwd_band_load(double &dst, const PlanDev &P, const FwdRow &R, int z, int p, int lane)
+{
+    if (P.variant == 1 && lane < 7 && in_band_b(p, R.y, z, R.m))
+        dst = P.store[9 * (int64_t)(R.boff + ((z == 1 || R.y == 1) ? p - 1 : (p == 1 ? 0 : 1))) + lane];
+}
+
 template <int K, bool EXACT, bool CONST_ROW, int SLOT>
 __device__ __forceinline__ void fwd_step(FwdRow &R, const PlanDev &P, const BatchArgs &A, int n, int z, int tau,
                                          const double *__restrict__ u, const double *__restrict__ f,
-                                         double *__restrict__ w, double *tab, int lane)
+                                         double *__restrict__ w, double *tab, double *sL, int lane)
 {
     if (!R.y) return;
     const int x = tau - R.start + 1;
@@ -269,6 +278,7 @@ __device__ __forceinline__ void fwd_step(FwdRow &R, const PlanDev &P, const Batc
         R.obc = (uint32_t)row_offset(n, z - 1, y) * 32u;
         R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
         R.otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
+        R.boff = P.variant == 1 ? P.bandoff[R.rid] : 0;
         smem_load_table<7, K>(tab, P.seedF + (int64_t)R.rid * 7 * K, lane);
         R.u_wm = u[R.oc];
         R.u_c = u[R.oc + 32];
@@ -284,9 +294,15 @@ __device__ __forceinline__ void fwd_step(FwdRow &R, const PlanDev &P, const Batc
         R.wprev = 0.0;
 #pragma unroll
         for (int q = 0; q < PF; ++q)
-            if (1 + q <= R.m) fwd_load(R.ring[(SLOT + q) % RING], u, f, w, R, 1 + q);
+            if (1 + q <= R.m) {
+                fwd_load(R.ring[(SLOT + q) % RING], u, f, w, R, 1 + q);
+                fwd_band_load(R.lring[(SLOT + q) % RING], P, R, z, 1 + q, lane);
+            }
     }
-    if (x + PF <= R.m) fwd_load(R.ring[(SLOT + PF) % RING], u, f, w, R, x + PF);
+    if (x + PF <= R.m) {
+        fwd_load(R.ring[(SLOT + PF) % RING], u, f, w, R, x + PF);
+        fwd_band_load(R.lring[(SLOT + PF) % RING], P, R, z, x + PF, lane);
+    }
     const FwdSlot &C = R.ring[SLOT];
     double ap[15];
     const double *a = A.arow;
@@ -314,17 +330,12 @@ __device__ __forceinline__ void fwd_step(FwdRow &R, const PlanDev &P, const Batc
     acc = madd<EXACT>(acc, a[14], R.utc_m);
     const double r = dsub(C.f, acc);
     R.ss = fma(r, r, R.ss);
-    // L entries: NDDF marchers (shared table) or the V1 band store
+    // L entries: lane m publishes L_m (band store or the shared NDDF table) to the warp
+    if (lane < 7) sL[lane] = (P.variant == 1 && in_band_b(x, R.y, z, R.m)) ? R.lring[SLOT] : tab[lane * K];
+    __syncwarp();
     double L[7];
-    const int y = R.y;
-    if (P.variant == 1 && in_band_b(x, y, z, R.m)) {
-        const double *st = P.store + 9 * (int64_t)band_idx_b(P, R.rid, x, y, z);
 #pragma unroll
-        for (int mm = 0; mm < 7; ++mm) L[mm] = st[mm];
-    } else {
-#pragma unroll
-        for (int mm = 0; mm < 7; ++mm) L[mm] = tab[mm * K];
-    }
+    for (int mm = 0; mm < 7; ++mm) L[mm] = sL[mm];
     double v;
     if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
         v = msub<true>(r, L[0], R.wprev);
@@ -369,6 +380,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
     __shared__ int s_ticket;
     __shared__ double s_red[BW][32];
     __shared__ double s_tab[BW][7 * K];
+    __shared__ double s_L[BW][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_ticket = atomicAdd(A.ticket, 1) + 1;  // counter starts at -1
     __syncthreads();
@@ -392,10 +404,10 @@ __global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
         R.ss = 0.0;
         __syncthreads();  // first window opened by the sync warp
         for (int tau0 = T0; tau0 <= T1; tau0 += BWIN) {
-            fwd_step<K, EXACT, CONST_ROW, 0>(R, P, A, n, z, tau0 + 0, u, f, w, tab, lane);
-            fwd_step<K, EXACT, CONST_ROW, 1>(R, P, A, n, z, tau0 + 1, u, f, w, tab, lane);
-            fwd_step<K, EXACT, CONST_ROW, 2>(R, P, A, n, z, tau0 + 2, u, f, w, tab, lane);
-            fwd_step<K, EXACT, CONST_ROW, 3>(R, P, A, n, z, tau0 + 3, u, f, w, tab, lane);
+            fwd_step<K, EXACT, CONST_ROW, 0>(R, P, A, n, z, tau0 + 0, u, f, w, tab, s_L[warp], lane);
+            fwd_step<K, EXACT, CONST_ROW, 1>(R, P, A, n, z, tau0 + 1, u, f, w, tab, s_L[warp], lane);
+            fwd_step<K, EXACT, CONST_ROW, 2>(R, P, A, n, z, tau0 + 2, u, f, w, tab, s_L[warp], lane);
+            fwd_step<K, EXACT, CONST_ROW, 3>(R, P, A, n, z, tau0 + 3, u, f, w, tab, s_L[warp], lane);
             __syncthreads();
         }
         s_red[warp][lane] = R.ss;
@@ -420,7 +432,11 @@ struct BwdSlot {
 
 struct BwdRow {
     int y, m, rid, bstart;  // bstart: backward step of the row's first point (x = m)
+    int qboff, qrow_band, qxe;  // lane m < 7: band offset / band-row flag / length of the row of q_m = p - d_m;
+                                // lane 7: the own row (1/D)
     uint32_t oc, on, ots, otc;
+    double lring[RING];   // lane m: prefetched value of L_m at q_m (lane 7: 1/D at p)
+    unsigned lsrc;        // 2 bits per slot: 0 = q outside the interior, 1 = band store, 2 = NDDF
     double wn_hi, wts_hi, wtc_hi, wprev;
     BwdSlot ring[RING];
 };
@@ -436,9 +452,30 @@ __device__ __forceinline__ void bwd_load(BwdSlot &S, const double *__restrict__ 
     S.u = u[R.oc + X];
 }
 
+// Lane m < 7 classifies q_m = p - d_m of point (x, y, z) and fetches its band-store entry L_m ahead
+// (_kernels.py:434-441 _lq); lane 7 does the same for 1/D at p.  Result: source code in R.lsrc.
+__device__ __forceinline__ void bwd_band_load(BwdRow &R, const PlanDev &P, int n, int z, int x, int lane, int SLOT)
+{
+    if (lane >= 8) return;
+    unsigned code = 2;
+    if (lane < 7) {
+        const int qx = x - kDX[lane], qy = R.y - kDY[lane], qz = z - kDZ[lane];
+        if (!interior(qx, qy, qz, n)) code = 0;
+        else if (P.variant == 1 && (R.qrow_band || qx == 1 || qx == R.qxe)) {
+            code = 1;
+            R.lring[SLOT] = P.store[9 * (int64_t)(R.qboff + (R.qrow_band ? qx - 1 : (qx == 1 ? 0 : 1))) + lane];
+        }
+    } else if (P.variant == 1 && in_band_b(x, R.y, z, R.m)) {
+        code = 1;
+        R.lring[SLOT] = P.store[9 * (int64_t)(R.qboff + ((z == 1 || R.y == 1) ? x - 1 : (x == 1 ? 0 : 1))) + 8];
+    }
+    R.lsrc = (R.lsrc & ~(3u << (2 * SLOT))) | (code << (2 * SLOT));
+}
+
 template <int K, bool EXACT, int SLOT>
 __device__ __forceinline__ void bwd_step(BwdRow &R, const PlanDev &P, const BatchArgs &A, int n, int z, int tau,
-                                         double *__restrict__ u, double *__restrict__ w, double *tab, int lane)
+                                         double *__restrict__ u, double *__restrict__ w, double *tab, double *sL,
+                                         int lane)
 {
     if (!R.y) return;
     const int k = tau - R.bstart;  // 0-based position along the descending row
@@ -451,6 +488,13 @@ __device__ __forceinline__ void bwd_step(BwdRow &R, const PlanDev &P, const Batc
         R.on = (uint32_t)row_offset(n, z, y + 1) * 32u;
         R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
         R.otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
+        if (lane < 8) {  // the row of q_m (lane m) or the own row (lane 7)
+            const int qy = lane < 7 ? y - kDY[lane] : y, qz = lane < 7 ? z - kDZ[lane] : z;
+            const bool valid = qy >= 1 && qz >= 1 && qy + qz <= n - 2;
+            R.qxe = n - 1 - qz - qy;
+            R.qrow_band = (qz == 1 || qy == 1);
+            R.qboff = (P.variant == 1 && valid) ? P.bandoff[row_id(n, qz, qy)] : 0;
+        }
         smem_load_table<8, K>(tab, P.seedB + (int64_t)R.rid * 8 * K, lane);
         const uint32_t M = (uint32_t)R.m * 32u;
         R.wn_hi = ldcg(w + R.on + M);
@@ -459,21 +503,26 @@ __device__ __forceinline__ void bwd_step(BwdRow &R, const PlanDev &P, const Batc
         R.wprev = 0.0;
 #pragma unroll
         for (int q = 0; q < PF; ++q)
-            if (R.m - q >= 1) bwd_load(R.ring[(SLOT + q) % RING], u, w, R, R.m - q);
+            if (R.m - q >= 1) {
+                bwd_load(R.ring[(SLOT + q) % RING], u, w, R, R.m - q);
+                bwd_band_load(R, P, n, z, R.m - q, lane, (SLOT + q) % RING);
+            }
     }
     const int x = R.m - k;
-    if (x - PF >= 1) bwd_load(R.ring[(SLOT + PF) % RING], u, w, R, x - PF);
+    if (x - PF >= 1) {
+        bwd_load(R.ring[(SLOT + PF) % RING], u, w, R, x - PF);
+        bwd_band_load(R, P, n, z, x - PF, lane, (SLOT + PF) % RING);
+    }
     const BwdSlot &C = R.ring[SLOT];
-    const bool band = P.variant == 1 && in_band_b(x, y, z, R.m);
-    const double inv_d = band ? P.store[9 * (int64_t)band_idx_b(P, R.rid, x, y, z) + 8] : tab[7 * K];
+    if (lane < 8) {
+        const unsigned code = (R.lsrc >> (2 * SLOT)) & 3u;
+        sL[lane] = code == 0 ? 0.0 : (code == 1 ? R.lring[SLOT] : tab[lane * K]);
+    }
+    __syncwarp();
     double Lq[7];
-    Lq[0] = lq_b(P, 0, x + 1, y, z, tab[0 * K]);
-    Lq[1] = lq_b(P, 1, x, y + 1, z, tab[1 * K]);
-    Lq[2] = lq_b(P, 2, x - 1, y + 1, z, tab[2 * K]);
-    Lq[3] = lq_b(P, 3, x + 1, y - 1, z + 1, tab[3 * K]);
-    Lq[4] = lq_b(P, 4, x, y - 1, z + 1, tab[4 * K]);
-    Lq[5] = lq_b(P, 5, x, y, z + 1, tab[5 * K]);
-    Lq[6] = lq_b(P, 6, x - 1, y, z + 1, tab[6 * K]);
+#pragma unroll
+    for (int mm = 0; mm < 7; ++mm) Lq[mm] = sL[mm];
+    const double inv_d = sL[7];
     double v = EXACT ? dmul(inv_d, C.wf) : inv_d * C.wf;
     if (EXACT) {  // reference order (_kernels.py:404-425)
         v = msub<true>(v, Lq[0], R.wprev);
@@ -511,6 +560,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
 {
     __shared__ int s_ticket;
     __shared__ double s_tab[BW][8 * K];
+    __shared__ double s_L[BW][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_ticket = atomicAdd(A.ticket, 1) + 1;
     __syncthreads();
@@ -530,14 +580,15 @@ __global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
     double *__restrict__ w = A.w + gb;
     double *tab = s_tab[warp];
     BwdRow R;
+    R.lsrc = 0;
     R.y = A.sched[zi].last[warp];
     R.bstart = R.y ? A.Tmax - (A.rows[row_id(n, z, R.y)].start + (n - 1 - z - R.y) - 1) : 0;
     __syncthreads();  // first window opened by the sync warp
     for (int tau0 = tb0; tau0 <= tb1; tau0 += BWIN) {
-        bwd_step<K, EXACT, 0>(R, P, A, n, z, tau0 + 0, u, w, tab, lane);
-        bwd_step<K, EXACT, 1>(R, P, A, n, z, tau0 + 1, u, w, tab, lane);
-        bwd_step<K, EXACT, 2>(R, P, A, n, z, tau0 + 2, u, w, tab, lane);
-        bwd_step<K, EXACT, 3>(R, P, A, n, z, tau0 + 3, u, w, tab, lane);
+        bwd_step<K, EXACT, 0>(R, P, A, n, z, tau0 + 0, u, w, tab, s_L[warp], lane);
+        bwd_step<K, EXACT, 1>(R, P, A, n, z, tau0 + 1, u, w, tab, s_L[warp], lane);
+        bwd_step<K, EXACT, 2>(R, P, A, n, z, tau0 + 2, u, w, tab, s_L[warp], lane);
+        bwd_step<K, EXACT, 3>(R, P, A, n, z, tau0 + 3, u, w, tab, s_L[warp], lane);
         __syncthreads();
     }
 }
