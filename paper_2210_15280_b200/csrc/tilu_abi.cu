@@ -159,10 +159,12 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
     // debug trace (TILU_TRACE=path): per CTA globaltimer stamps of the last sweep's passes
     static const char *trace_path = std::getenv("TILU_TRACE");
     unsigned long long *trace = nullptr;
-    const size_t ntrace = 2 * 4 * (size_t)G * nl;
+    const size_t ntrace = 2 * 8 * (size_t)G * nl;
     if (trace_path) trace = reinterpret_cast<unsigned long long *>(sc.get(ntrace));
     BatchArgs A{};
     A.trace = nullptr;
+    static const char *mt = std::getenv("TILU_DEBUG_MAX_TICKET");
+    A.max_ticket = mt ? std::atoi(mt) : -1;
     A.u = up;
     A.f = fp;
     A.w = wp;
@@ -185,7 +187,7 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
         A.ticket = sync + 1;
         A.flags = sync + 2 + (size_t)G * nl;
         A.part = nullptr;
-        A.trace = trace ? trace + 4 * (size_t)G * nl : nullptr;
+        A.trace = trace ? trace + 8 * (size_t)G * nl : nullptr;
         prof_begin(s);
         ok = ok && launch_batch_pass(P, A, exact, false, s);
         prof_end("batch_bwd", s);
@@ -201,7 +203,7 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
         cudaMemcpyAsync(h.data(), trace, ntrace * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
         if (FILE *fh = std::fopen(trace_path, "wb")) {
-            const int hdr[3] = {G, nl, 4};
+            const int hdr[3] = {G, nl, 8};
             std::fwrite(hdr, sizeof(int), 3, fh);
             std::fwrite(h.data(), sizeof(unsigned long long), ntrace, fh);
             std::fclose(fh);

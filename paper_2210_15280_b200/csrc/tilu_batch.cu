@@ -74,13 +74,17 @@ __device__ __forceinline__ unsigned long long gtimer()
     return t;
 }
 
+// trace layout per CTA (8 x u64): start ns, first-window-open ns, end ns, sync-warp dependency-wait
+// cycles, sync-warp release (MEMBAR) cycles, warp-0 barrier-wait cycles, warp-0 step cycles, windows
+constexpr int TRACE_W = 8;
+
 __device__ __forceinline__ void sync_warp_loop(int *myflag, const int *dep, int depEnd, int D, int t0, int t1,
                                                unsigned long long *trace)
 {
     // everything a window starting at tau0 reads from the neighbouring layer (including the PF-ahead
     // prefetches) has step <= tau0 + BWIN + PF - 2 - D; the neighbour never publishes past depEnd
     const bool leader = (threadIdx.x & 31) == 0;
-    unsigned long long waited = 0;
+    unsigned long long waited = 0, released = 0, nwin = 0;
     if (trace && leader) trace[0] = gtimer();
     if (leader && dep) wait_progress(dep, min(t0 + BWIN + PF - 2 - D, depEnd));
     if (trace && leader) trace[1] = gtimer();
@@ -88,16 +92,23 @@ __device__ __forceinline__ void sync_warp_loop(int *myflag, const int *dep, int 
     for (int tau0 = t0; tau0 <= t1; tau0 += BWIN) {
         const int tau1 = tau0 + BWIN;
         if (leader && dep && tau1 <= t1) {
-            const unsigned long long a = trace ? gtimer() : 0;
+            const long long a = trace ? clock64() : 0;
             wait_progress(dep, min(tau1 + BWIN + PF - 2 - D, depEnd));
-            if (trace) waited += gtimer() - a;
+            if (trace) waited += clock64() - a;
         }
         __syncthreads();  // closes this window / opens the next
-        if (leader) st_release(myflag, min(tau1, t1 + 1) - 1);  // MEMBAR.GPU + store, cumulative over the barrier
+        if (leader) {
+            const long long a = trace ? clock64() : 0;
+            st_release(myflag, min(tau1, t1 + 1) - 1);  // MEMBAR.GPU + store, cumulative over the barrier
+            if (trace) released += clock64() - a;
+        }
+        ++nwin;
     }
     if (trace && leader) {
         trace[2] = gtimer();
         trace[3] = waited;
+        trace[4] = released;
+        trace[7] = nwin;
     }
 }
 
@@ -188,6 +199,9 @@ __device__ __forceinline__ void smem_load_table(double *tab, const double *__res
 template <int M, int K>
 __device__ __forceinline__ void smem_march(double *tab, int lane)
 {
+#ifdef TILU_ABLATE_NOMARCH
+    return;
+#endif
     constexpr int NE = M * (K - 1);
     if (NE == 0) return;
     constexpr int IT = NE > 0 ? (NE + 31) / 32 : 1;
@@ -239,6 +253,11 @@ __device__ __forceinline__ void fwd_load(FwdSlot &S, const double *__restrict__ 
                                          const double *__restrict__ w, const FwdRow &R, int p)
 {
     const uint32_t X = (uint32_t)p * 32u;
+#ifdef TILU_ABLATE_NOLOAD
+    S.ue = X * 1e-9; S.us = S.ue + 1; S.un = S.ue + 2; S.ubn = S.ue + 3; S.ubc = S.ue + 4; S.uts = S.ue + 5;
+    S.utc = S.ue + 6; S.f = S.ue + 7; S.ws = S.ue + 8; S.wbn = S.ue + 9; S.wbc = S.ue + 10;
+    return;
+#endif
     S.ue = u[R.oc + X + 32];
     S.us = u[R.os + X + 32];
     S.un = u[R.on + X];
@@ -259,124 +278,11 @@ __device__ __forceinline__ void fwd_band_load(double &dst, const PlanDev &P, con
         dst = P.store[9 * (int64_t)(R.boff + ((z == 1 || R.y == 1) ? p - 1 : (p == 1 ? 0 : 1))) + lane];
 }
 
-template <int K, bool EXACT, bool CONST_ROW, int SLOT>
-__device__ __forceinline__ void fwd_step(FwdRow &R, const PlanDev &P, const BatchArgs &A, int n, int z, int tau,
-                                         const double *__restrict__ u, const double *__restrict__ f,
-                                         double *__restrict__ w, double *tab, double *sL, int lane)
-{
-    if (!R.y) return;
-    const int x = tau - R.start + 1;
-    if (x < 1) return;
-    if (x == 1) {  // row start: offsets, seed table, windows, ring fill for points 1..PF
-        const int y = R.y;
-        R.m = n - 1 - z - y;
-        R.rid = row_id(n, z, y);
-        R.oc = (uint32_t)row_offset(n, z, y) * 32u;
-        R.os = (uint32_t)row_offset(n, z, y - 1) * 32u;
-        R.on = (uint32_t)row_offset(n, z, y + 1) * 32u;
-        R.obn = (uint32_t)row_offset(n, z - 1, y + 1) * 32u;
-        R.obc = (uint32_t)row_offset(n, z - 1, y) * 32u;
-        R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
-        R.otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
-        R.boff = P.variant == 1 ? P.bandoff[R.rid] : 0;
-        smem_load_table<7, K>(tab, P.seedF + (int64_t)R.rid * 7 * K, lane);
-        R.u_wm = u[R.oc];
-        R.u_c = u[R.oc + 32];
-        R.us0 = u[R.os + 32];
-        R.un_m = u[R.on];
-        R.ubn_m = u[R.obn];
-        R.ubc0 = u[R.obc + 32];
-        R.uts0 = u[R.ots + 32];
-        R.utc_m = u[R.otc];
-        R.ws0 = ldcg(w + R.os + 32);
-        R.wbn_m = ldcg(w + R.obn);
-        R.wbc0 = ldcg(w + R.obc + 32);
-        R.wprev = 0.0;
-#pragma unroll
-        for (int q = 0; q < PF; ++q)
-            if (1 + q <= R.m) {
-                fwd_load(R.ring[(SLOT + q) % RING], u, f, w, R, 1 + q);
-                fwd_band_load(R.lring[(SLOT + q) % RING], P, R, z, 1 + q, lane);
-            }
-    }
-    if (x + PF <= R.m) {
-        fwd_load(R.ring[(SLOT + PF) % RING], u, f, w, R, x + PF);
-        fwd_band_load(R.lring[(SLOT + PF) % RING], P, R, z, x + PF, lane);
-    }
-    const FwdSlot &C = R.ring[SLOT];
-    double ap[15];
-    const double *a = A.arow;
-    if (!CONST_ROW) {
-        const double *ar = P.arows + 15 * (int64_t)(R.oc / 32u + x);
-#pragma unroll
-        for (int i = 0; i < 15; ++i) ap[i] = ar[i];
-        a = ap;
-    }
-    // residual in stencil_apply order (_kernels.py:255-266), then f - A u
-    double acc = EXACT ? dmul(a[7], R.u_c) : a[7] * R.u_c;
-    acc = madd<EXACT>(acc, a[0], R.u_wm);
-    acc = madd<EXACT>(acc, a[1], R.us0);
-    acc = madd<EXACT>(acc, a[2], C.us);
-    acc = madd<EXACT>(acc, a[3], R.ubn_m);
-    acc = madd<EXACT>(acc, a[4], C.ubn);
-    acc = madd<EXACT>(acc, a[5], R.ubc0);
-    acc = madd<EXACT>(acc, a[6], C.ubc);
-    acc = madd<EXACT>(acc, a[8], C.ue);
-    acc = madd<EXACT>(acc, a[9], C.un);
-    acc = madd<EXACT>(acc, a[10], R.un_m);
-    acc = madd<EXACT>(acc, a[11], C.uts);
-    acc = madd<EXACT>(acc, a[12], R.uts0);
-    acc = madd<EXACT>(acc, a[13], C.utc);
-    acc = madd<EXACT>(acc, a[14], R.utc_m);
-    const double r = dsub(C.f, acc);
-    R.ss = fma(r, r, R.ss);
-    // L entries: lane m publishes L_m (band store or the shared NDDF table) to the warp
-    if (lane < 7) sL[lane] = (P.variant == 1 && in_band_b(x, R.y, z, R.m)) ? R.lring[SLOT] : tab[lane * K];
-    __syncwarp();
-    double L[7];
-#pragma unroll
-    for (int mm = 0; mm < 7; ++mm) L[mm] = sL[mm];
-    double v;
-    if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
-        v = msub<true>(r, L[0], R.wprev);
-        v = msub<true>(v, L[1], R.ws0);
-        v = msub<true>(v, L[2], C.ws);
-        v = msub<true>(v, L[3], R.wbn_m);
-        v = msub<true>(v, L[4], C.wbn);
-        v = msub<true>(v, L[5], R.wbc0);
-        v = msub<true>(v, L[6], C.wbc);
-    } else {  // own-row term last: one FMA on the row's dependency chain
-        v = msub<false>(r, L[1], R.ws0);
-        v = msub<false>(v, L[2], C.ws);
-        v = msub<false>(v, L[3], R.wbn_m);
-        v = msub<false>(v, L[4], C.wbn);
-        v = msub<false>(v, L[5], R.wbc0);
-        v = msub<false>(v, L[6], C.wbc);
-        v = msub<false>(v, L[0], R.wprev);
-    }
-    w[R.oc + (uint32_t)x * 32u] = v;
-    smem_march<7, K>(tab, lane);
-    R.u_wm = R.u_c;
-    R.u_c = C.ue;
-    R.us0 = C.us;
-    R.un_m = C.un;
-    R.ubn_m = C.ubn;
-    R.ubc0 = C.ubc;
-    R.uts0 = C.uts;
-    R.utc_m = C.utc;
-    R.ws0 = C.ws;
-    R.wbn_m = C.wbn;
-    R.wbc0 = C.wbc;
-    R.wprev = v;
-    if (x == R.m) {
-        R.y = A.rows[R.rid].next;
-        if (R.y) R.start = A.rows[row_id(n, z, R.y)].start;
-    }
-}
-
 template <int K, bool EXACT, bool CONST_ROW>
-__global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
 {
+    // Rolled step loop with a current / next load buffer (one point of prefetch): smaller code and
+    // register footprint than the unrolled ring, which lets two CTAs (18 warps) share an SM.
     __shared__ int s_ticket;
     __shared__ double s_red[BW][32];
     __shared__ double s_tab[BW][7 * K];
@@ -384,6 +290,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_ticket = atomicAdd(A.ticket, 1) + 1;  // counter starts at -1
     __syncthreads();
+    if (A.max_ticket >= 0 && s_ticket > A.max_ticket) return;
     const int nl = P.n - 3;
     const int zi = s_ticket / A.G, g = s_ticket - (s_ticket / A.G) * A.G;
     const int n = P.n, z = zi + 1;
@@ -391,23 +298,126 @@ __global__ void __launch_bounds__(NT, 1) k_batch_fwd(PlanDev P, BatchArgs A)
     int *myflag = A.flags + g * nl + zi;
     if (warp == BW) {
         sync_warp_loop(myflag, z > 1 ? myflag - 1 : nullptr, z > 1 ? A.sched[zi - 1].T1 : 0, A.D, T0, T1,
-                       A.trace ? A.trace + 4 * (size_t)s_ticket : nullptr);
+                       A.trace ? A.trace + TRACE_W * (size_t)s_ticket : nullptr);
     } else {
         const size_t gb = (size_t)g * P.grid * 32 + lane;
         const double *__restrict__ u = A.u + gb;
         const double *__restrict__ f = A.f + gb;
         double *__restrict__ w = A.w + gb;
         double *tab = s_tab[warp];
+        double *sL = s_L[warp];
         FwdRow R;
         R.y = A.sched[zi].first[warp];
         R.start = R.y ? A.rows[row_id(n, z, R.y)].start : 0;
         R.ss = 0.0;
+        FwdSlot C{}, N{};
+        double cband = 0.0, nband = 0.0;
         __syncthreads();  // first window opened by the sync warp
         for (int tau0 = T0; tau0 <= T1; tau0 += BWIN) {
-            fwd_step<K, EXACT, CONST_ROW, 0>(R, P, A, n, z, tau0 + 0, u, f, w, tab, s_L[warp], lane);
-            fwd_step<K, EXACT, CONST_ROW, 1>(R, P, A, n, z, tau0 + 1, u, f, w, tab, s_L[warp], lane);
-            fwd_step<K, EXACT, CONST_ROW, 2>(R, P, A, n, z, tau0 + 2, u, f, w, tab, s_L[warp], lane);
-            fwd_step<K, EXACT, CONST_ROW, 3>(R, P, A, n, z, tau0 + 3, u, f, w, tab, s_L[warp], lane);
+            for (int tau = tau0; tau < tau0 + BWIN; ++tau) {
+                if (!R.y) break;
+                const int x = tau - R.start + 1;
+                if (x < 1) continue;
+                if (x == 1) {  // row start: offsets, seed table, windows, point-1 values
+                    const int y = R.y;
+                    R.m = n - 1 - z - y;
+                    R.rid = row_id(n, z, y);
+                    R.oc = (uint32_t)row_offset(n, z, y) * 32u;
+                    R.os = (uint32_t)row_offset(n, z, y - 1) * 32u;
+                    R.on = (uint32_t)row_offset(n, z, y + 1) * 32u;
+                    R.obn = (uint32_t)row_offset(n, z - 1, y + 1) * 32u;
+                    R.obc = (uint32_t)row_offset(n, z - 1, y) * 32u;
+                    R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
+                    R.otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
+                    R.boff = P.variant == 1 ? P.bandoff[R.rid] : 0;
+                    smem_load_table<7, K>(tab, P.seedF + (int64_t)R.rid * 7 * K, lane);
+                    R.u_wm = u[R.oc];
+                    R.u_c = u[R.oc + 32];
+                    R.us0 = u[R.os + 32];
+                    R.un_m = u[R.on];
+                    R.ubn_m = u[R.obn];
+                    R.ubc0 = u[R.obc + 32];
+                    R.uts0 = u[R.ots + 32];
+                    R.utc_m = u[R.otc];
+                    R.ws0 = ldcg(w + R.os + 32);
+                    R.wbn_m = ldcg(w + R.obn);
+                    R.wbc0 = ldcg(w + R.obc + 32);
+                    R.wprev = 0.0;
+                    fwd_load(C, u, f, w, R, 1);
+                    fwd_band_load(cband, P, R, z, 1, lane);
+                }
+                // prefetch point x+1 (branch-free: at the row end it re-reads point m, unused)
+                const int pp = min(x + 1, R.m);
+                fwd_load(N, u, f, w, R, pp);
+                fwd_band_load(nband, P, R, z, pp, lane);
+                double ap[15];
+                const double *a = A.arow;
+                if (!CONST_ROW) {
+                    const double *ar = P.arows + 15 * (int64_t)(R.oc / 32u + x);
+#pragma unroll
+                    for (int i = 0; i < 15; ++i) ap[i] = ar[i];
+                    a = ap;
+                }
+                // residual in stencil_apply order (_kernels.py:255-266), then f - A u
+                double acc = EXACT ? dmul(a[7], R.u_c) : a[7] * R.u_c;
+                acc = madd<EXACT>(acc, a[0], R.u_wm);
+                acc = madd<EXACT>(acc, a[1], R.us0);
+                acc = madd<EXACT>(acc, a[2], C.us);
+                acc = madd<EXACT>(acc, a[3], R.ubn_m);
+                acc = madd<EXACT>(acc, a[4], C.ubn);
+                acc = madd<EXACT>(acc, a[5], R.ubc0);
+                acc = madd<EXACT>(acc, a[6], C.ubc);
+                acc = madd<EXACT>(acc, a[8], C.ue);
+                acc = madd<EXACT>(acc, a[9], C.un);
+                acc = madd<EXACT>(acc, a[10], R.un_m);
+                acc = madd<EXACT>(acc, a[11], C.uts);
+                acc = madd<EXACT>(acc, a[12], R.uts0);
+                acc = madd<EXACT>(acc, a[13], C.utc);
+                acc = madd<EXACT>(acc, a[14], R.utc_m);
+                const double r = dsub(C.f, acc);
+                R.ss = fma(r, r, R.ss);
+                // L entries: lane m publishes L_m (band store or the shared NDDF table)
+                if (lane < 7) sL[lane] = (P.variant == 1 && in_band_b(x, R.y, z, R.m)) ? cband : tab[lane * K];
+                __syncwarp();
+                double v;
+                if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
+                    v = msub<true>(r, sL[0], R.wprev);
+                    v = msub<true>(v, sL[1], R.ws0);
+                    v = msub<true>(v, sL[2], C.ws);
+                    v = msub<true>(v, sL[3], R.wbn_m);
+                    v = msub<true>(v, sL[4], C.wbn);
+                    v = msub<true>(v, sL[5], R.wbc0);
+                    v = msub<true>(v, sL[6], C.wbc);
+                } else {  // own-row term last: one FMA on the row's dependency chain
+                    v = msub<false>(r, sL[1], R.ws0);
+                    v = msub<false>(v, sL[2], C.ws);
+                    v = msub<false>(v, sL[3], R.wbn_m);
+                    v = msub<false>(v, sL[4], C.wbn);
+                    v = msub<false>(v, sL[5], R.wbc0);
+                    v = msub<false>(v, sL[6], C.wbc);
+                    v = msub<false>(v, sL[0], R.wprev);
+                }
+                w[R.oc + (uint32_t)x * 32u] = v;
+                smem_march<7, K>(tab, lane);
+                R.u_wm = R.u_c;
+                R.u_c = C.ue;
+                R.us0 = C.us;
+                R.un_m = C.un;
+                R.ubn_m = C.ubn;
+                R.ubc0 = C.ubc;
+                R.uts0 = C.uts;
+                R.utc_m = C.utc;
+                R.ws0 = C.ws;
+                R.wbn_m = C.wbn;
+                R.wbc0 = C.wbc;
+                R.wprev = v;
+                C = N;
+                cband = nband;
+                if (x == R.m) {
+                    R.y = A.rows[R.rid].next;
+                    if (R.y) R.start = A.rows[row_id(n, z, R.y)].start;
+                }
+            }
             __syncthreads();
         }
         s_red[warp][lane] = R.ss;
@@ -509,11 +519,7 @@ __device__ __forceinline__ void bwd_step(BwdRow &R, const PlanDev &P, const Batc
             }
     }
     const int x = R.m - k;
-    if (x - PF >= 1) {
-        bwd_load(R.ring[(SLOT + PF) % RING], u, w, R, x - PF);
-        bwd_band_load(R, P, n, z, x - PF, lane, (SLOT + PF) % RING);
-    }
-    const BwdSlot &C = R.ring[SLOT];
+    const BwdSlot C = R.ring[SLOT];
     if (lane < 8) {
         const unsigned code = (R.lsrc >> (2 * SLOT)) & 3u;
         sL[lane] = code == 0 ? 0.0 : (code == 1 ? R.lring[SLOT] : tab[lane * K]);
@@ -544,6 +550,11 @@ __device__ __forceinline__ void bwd_step(BwdRow &R, const PlanDev &P, const Batc
     const uint32_t X = (uint32_t)x * 32u;
     w[R.oc + X] = v;
     u[R.oc + X] = dadd(C.u, v);
+    {   // prefetch point x-PF (branch-free: below x = 1 the loads re-read point 1, unused)
+        const int pp = max(x - PF, 1);
+        bwd_load(R.ring[(SLOT + PF) % RING], u, w, R, pp);
+        bwd_band_load(R, P, n, z, pp, lane, (SLOT + PF) % RING);
+    }
     smem_march<8, K>(tab, lane);
     R.wn_hi = C.wn;
     R.wts_hi = C.wts;
@@ -556,7 +567,7 @@ __device__ __forceinline__ void bwd_step(BwdRow &R, const PlanDev &P, const Batc
 }
 
 template <int K, bool EXACT>
-__global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(NT, 2) k_batch_bwd(PlanDev P, BatchArgs A)
 {
     __shared__ int s_ticket;
     __shared__ double s_tab[BW][8 * K];
@@ -572,7 +583,7 @@ __global__ void __launch_bounds__(NT, 1) k_batch_bwd(PlanDev P, BatchArgs A)
     const int tb0 = A.Tmax - A.sched[zi].T1, tb1 = A.Tmax - A.sched[zi].T0;
     if (warp == BW) {
         sync_warp_loop(myflag, z < nl ? myflag + 1 : nullptr, z < nl ? A.Tmax - A.sched[zi + 1].T0 : 0, A.D, tb0,
-                       tb1, A.trace ? A.trace + 4 * (size_t)s_ticket : nullptr);
+                       tb1, A.trace ? A.trace + TRACE_W * (size_t)s_ticket : nullptr);
         return;
     }
     const size_t gb = (size_t)g * P.grid * 32 + lane;

@@ -9,7 +9,7 @@ namespace tilu {
 constexpr int BW = 8;        // compute warps per CTA = rows of one z-layer in flight
 constexpr int NT = (BW + 1) * 32;  // + one sync warp (progress wait / publish off the compute path)
 constexpr int BWIN = 4;      // synchronisation window (steps between CTA barriers)
-constexpr int PF = 3;        // load prefetch distance (points)
+constexpr int PF = 1;        // load prefetch distance (points)
 constexpr int RING = 4;      // register ring slots (== BWIN: static slot indices in the unrolled window)
 static_assert(RING == BWIN && PF < RING, "ring layout");
 // min. start offset of consecutive rows of a layer: window + 1 + PF
@@ -39,6 +39,7 @@ struct BatchArgs {
     double *part;  // [G][n-3][32] residual partial sums or nullptr
     unsigned long long *trace;  // debug: per CTA [ticket][4] globaltimer stamps (start, first window open,
                                 //        end, windows) or nullptr
+    int max_ticket;   // debug: CTAs with a larger ticket exit at once (-1 = off)
     double arow[15];  // constant stencil (kernel-parameter constant bank: DMUL operands, no registers)
 };
 
