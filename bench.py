@@ -155,15 +155,18 @@ def peaks() -> dict:
         return {}
 
 
-def algo_bytes(level: int, nband: int, variant: str) -> dict:
-    """Algorithmic bytes per interior DoF of each kernel family (SURVEY 8d fixed model:
-    vectors once per pass, V1 band rows once per pass, stencil/coefficients free)."""
+def algo_bytes(level: int, nband: int, variant: str, shared_surrogate: bool = True) -> dict:
+    """Algorithmic bytes per interior DoF.  "sweep" is SURVEY 8(d)'s fixed model (vectors once per
+    pass, plus each tet's V1 band rows once per pass).  The per-kernel figures count what a kernel
+    must move: the batched kernels share ONE band store among all tets of a group (read once per
+    layer CTA, L2-resident), so their per-DoF band share is ~0."""
     from paper_2210_15280_b200 import lattice
     N = lattice.interior_size(level)
     band = 72.0 * nband / N if variant == "v1" else 0.0
+    kb = 0.0 if shared_surrogate else band
     return {
         "sweep": 48.0 + 2 * band,
-        "plane_fwd": 24.0 + band, "plane_bwd": 24.0 + band,      # fused passes: u,f->w ; w,u->u
+        "batch_fwd": 24.0 + kb, "batch_bwd": 24.0 + kb,      # fused passes: u,f -> w ; w,u -> u
         "residual": 24.0, "simple_fwd": 16.0 + band, "simple_bwd": 24.0 + band,
     }
 
