@@ -112,14 +112,6 @@ int tilu_unpack(const tilu_plan_t *plan, const double *src, double *dst, int nte
 int tilu_sweep_packed(const tilu_plan_t *plan, double *u_p, const double *f_p, double *w_p, int ntets, int sweeps,
                       double *rnorm2, void *stream);
 
-/* Host-only introspection of the batched path's greedy schedule of a level for synchronisation
- * window `bwin` and load prefetch distance `pf` (steps / points; plans use 4 and 3):
- * per interior row (row_id order: z, then y) its forward start step and owning warp; per z-layer its
- * last step; the cross-layer slack D and the last step Tmax.  Returns the number of rows or a
- * negative status. */
-int tilu_batch_schedule(int level, int bwin, int pf, int *row_start, int *row_warp, int *layer_T1, int *D,
-                        int *Tmax);
-
 /* Stored-factor comparison (plan built with desc.factors): CellILU.solve_into (ilu.py:225-227)
  * = _kernels.ilu_forward (_kernels.py:150-166) + ilu_backward (:169-192), and the sweep. */
 int tilu_stored_solve_into(const tilu_plan_t *plan, double *w, int ntets, void *stream);

@@ -46,7 +46,7 @@ EXPORTS = (
     "tilu_stored_solve_into", "tilu_stored_sweep", "tilu_factorize_stream", "tilu_last_error",
     "tilu_version", "tilu_last_launch_count", "tilu_plan_grid_size", "tilu_plan_interior_size",
     "tilu_profile_enable", "tilu_profile_reset", "tilu_profile_read", "tilu_packed_size", "tilu_pack",
-    "tilu_unpack", "tilu_sweep_packed", "tilu_batch_schedule",
+    "tilu_unpack", "tilu_sweep_packed",
 )
 
 
@@ -89,8 +89,6 @@ def lib():
         getattr(L, name).restype = _I
     L.tilu_sweep_packed.argtypes = [_P, _P, _P, _P, _I, _I, _P, _P]
     L.tilu_sweep_packed.restype = _I
-    L.tilu_batch_schedule.argtypes = [_I, _I, _I, _P, _P, _P, _P, _P]
-    L.tilu_batch_schedule.restype = _I
     L.tilu_profile_enable.argtypes = [_I]
     L.tilu_profile_enable.restype = None
     L.tilu_profile_reset.restype = None
@@ -126,19 +124,3 @@ def profile_read() -> dict:
         nm = names.raw[64 * i:64 * (i + 1)].split(b"\0", 1)[0].decode()
         out[nm] = (int(counts[i]), float(ms[i]))
     return out
-
-
-def batch_schedule(level: int, bwin: int = 4, pf: int = 3) -> dict:
-    """The batched path's greedy schedule as computed by libtilu (host only): per row
-    (row_id order) forward start step and warp, per layer last step, D, Tmax."""
-    import numpy as np
-    n = 2 ** level
-    nrows = (n - 3) * (n - 2) // 2
-    start, warp = np.zeros(max(nrows, 1), np.int32), np.zeros(max(nrows, 1), np.int32)
-    T1 = np.zeros(max(n - 3, 1), np.int32)
-    D, Tmax = ctypes.c_int(), ctypes.c_int()
-    k = lib().tilu_batch_schedule(level, bwin, pf, start.ctypes.data, warp.ctypes.data, T1.ctypes.data, ctypes.byref(D),
-                                  ctypes.byref(Tmax))
-    if k < 0:
-        check(-k)
-    return {"start": start[:k], "warp": warp[:k], "T1": T1[:n - 3], "D": D.value, "Tmax": Tmax.value, "bwin": bwin, "pf": pf}

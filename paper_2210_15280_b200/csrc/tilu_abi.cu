@@ -150,19 +150,13 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
     const PlanDev &P = p->dev;
     const int G = (ntets + 31) / 32, nl = P.n - 3;
     Scratch sc(s);
-    // sync block: [ticket_f, ticket_b, flags_f[G*nl], flags_b[G*nl]] as ints, reset to -1 per sweep
-    const size_t nsync = 2 + 2 * (size_t)G * nl;
-    int *sync = reinterpret_cast<int *>(sc.get((nsync + 1) / 2));
+    // sync block per pass: [ticket, pad, progress[G][nl][GSTRIDE]] ints, zeroed before each pass
+    const size_t npass = 4 + (size_t)G * nl * GSTRIDE;
+    int *sync = reinterpret_cast<int *>(sc.get(npass));  // 2 passes' worth of ints (npass doubles)
     double *part = rnorm2 ? sc.get((size_t)G * nl * 32) : nullptr;
     if (!sync || (rnorm2 && !part)) return fail(TILU_ENOMEM, "scratch allocation failed");
     const bool exact = !(p->flags & TILU_FAST);
-    // debug trace (TILU_TRACE=path): per CTA globaltimer stamps of the last sweep's passes
-    static const char *trace_path = std::getenv("TILU_TRACE");
-    unsigned long long *trace = nullptr;
-    const size_t ntrace = 2 * 8 * (size_t)G * nl;
-    if (trace_path) trace = reinterpret_cast<unsigned long long *>(sc.get(ntrace));
     BatchArgs A{};
-    A.trace = nullptr;
     static const char *mt = std::getenv("TILU_DEBUG_MAX_TICKET");
     A.max_ticket = mt ? std::atoi(mt) : -1;
     A.u = up;
@@ -170,24 +164,18 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
     A.w = wp;
     A.G = G;
     A.ntets = ntets;
-    A.sched = static_cast<const LayerSched *>(p->bsched);
-    A.rows = static_cast<const RowSched *>(p->brows);
-    A.Tmax = p->bTmax;
-    A.D = p->bD;
     std::memcpy(A.arow, p->harow, sizeof(A.arow));
     for (int k = 0; k < sweeps; ++k) {
-        cudaMemsetAsync(sync, 0xFF, nsync * sizeof(int), s);
+        cudaMemsetAsync(sync, 0, 2 * npass * sizeof(int), s);
         A.ticket = sync;
-        A.flags = sync + 2;
+        A.gprog = sync + 4;
         A.part = part;
-        A.trace = trace;
         prof_begin(s);
         bool ok = launch_batch_pass(P, A, exact, true, s);
         prof_end("batch_fwd", s);
-        A.ticket = sync + 1;
-        A.flags = sync + 2 + (size_t)G * nl;
+        A.ticket = sync + npass;
+        A.gprog = sync + npass + 4;
         A.part = nullptr;
-        A.trace = trace ? trace + 8 * (size_t)G * nl : nullptr;
         prof_begin(s);
         ok = ok && launch_batch_pass(P, A, exact, false, s);
         prof_end("batch_bwd", s);
@@ -198,20 +186,8 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
             ++g_launches;
         }
     }
-    if (trace) {
-        std::vector<unsigned long long> h(ntrace);
-        cudaMemcpyAsync(h.data(), trace, ntrace * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
-        if (FILE *fh = std::fopen(trace_path, "wb")) {
-            const int hdr[3] = {G, nl, 8};
-            std::fwrite(hdr, sizeof(int), 3, fh);
-            std::fwrite(h.data(), sizeof(unsigned long long), ntrace, fh);
-            std::fclose(fh);
-        }
-    }
     return TILU_OK;
 }
-
 
 extern "C" {
 
@@ -396,22 +372,7 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
         }
         P.seedA = dseedA;
     }
-    {
-        std::vector<LayerSched> sch;
-        std::vector<RowSched> rsch;
-        int T = 0, D = 0;
-        batch_schedule(n, BWIN, PF, sch, rsch, T, D);
-        LayerSched *dsch = nullptr;
-        RowSched *drs = nullptr;
-        if ((rc = dev_upload(p, &dsch, sch.data(), sch.size())) || (rc = dev_upload(p, &drs, rsch.data(), rsch.size()))) {
-            tilu_plan_destroy(p);
-            return rc;
-        }
-        p->bsched = dsch;
-        p->brows = drs;
-        p->bTmax = T;
-        p->bD = D;
-    }
+    p->bsched = (n - 3 <= MAXR) ? reinterpret_cast<const void *>(1) : nullptr;  // batched path supports this level
     launch_seed(P, dl, dd, dseedF, dseedB, 0);
     if (d->acoefs) launch_seed_op(P, dacoefs, d->aky1, d->akz1, dseedA, 0);
     if (cudaDeviceSynchronize() != cudaSuccess || (rc = check_cuda("seed tables"))) {
@@ -543,25 +504,6 @@ static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int nt
         g_launches += 2;
     }
     return check_cuda("sweep");
-}
-
-int tilu_batch_schedule(int level, int bwin, int pf, int *row_start, int *row_warp, int *layer_T1, int *D, int *Tmax)
-{
-    if (level < 2 || level > 10) return -fail(TILU_EINVAL, "level %d outside 2..10", level);
-    if (bwin < 1 || bwin > 64 || pf < 0 || pf > 16) return -fail(TILU_EINVAL, "window / prefetch out of range");
-    const int n = 1 << level;
-    std::vector<LayerSched> sch;
-    std::vector<RowSched> rs;
-    batch_schedule(n, bwin, pf, sch, rs, *Tmax, *D);
-    for (int z = 1; z <= n - 3; ++z) {
-        layer_T1[z - 1] = sch[z - 1].T1;
-        for (int wi = 0; wi < BW; ++wi)
-            for (int y = sch[z - 1].first[wi]; y; y = rs[row_id(n, z, y)].next) {
-                row_start[row_id(n, z, y)] = rs[row_id(n, z, y)].start;
-                row_warp[row_id(n, z, y)] = wi;
-            }
-    }
-    return (n - 3) * (n - 2) / 2;
 }
 
 int64_t tilu_packed_size(const tilu_plan_t *p, int ntets)

@@ -7,22 +7,21 @@
 // coalesced 256 B access, no lane is ever idle, and each lane executes exactly the reference's
 // serial operation sequence for its own tet (bitwise parity in exact mode).
 //
-// Schedule: one CTA per (group, z-layer), BW warps per CTA, each warp owns one row of the layer
-// at a time.  A host-side greedy list schedule (batch_schedule below) gives every row (y, z) a
-// start step S: point (x, y, z) runs at forward step S + x - 1, rows start in y order as soon as
-//   * a warp of the CTA is free,
-//   * S(y) >= S(y-1) + AMIN: row y reads row y-1 (same layer, another warp) only from
-//     synchronisation windows already closed by a CTA barrier, even one point ahead (prefetch);
-//     the CTA therefore synchronises once per BWIN steps, not per step;
-//   * S_z(y) >= S_{z-1}(y+1) + 1 + D and >= S_{z-1}(y) + 2 + D: everything read from the layer
-//     below (another CTA, usually another SM) was produced >= D + 1 steps earlier.  Layers hand
-//     over through release/acquire progress counters published at every window end; D is slack
-//     so the consumer rarely waits.
-// The backward pass runs the exact time reversal of this schedule (T_b = Tmax - T), which
-// satisfies the transposed dependencies.  CTAs take (group, layer) tickets in layer order
-// (ascending z forward, descending backward), so a CTA only ever waits for CTAs that already
-// hold earlier tickets: no deadlock whatever the residency.  tests/test_schedule.py verifies
-// dependencies, warp exclusivity and handoff completion on the host.
+// Execution: dataflow, no barriers on the compute path.  One CTA per (group, z-layer); CTAs take
+// tickets in dependency order (ascending z forward, descending backward), so a CTA only ever
+// waits for CTAs that already run: deadlock-free for any residency.  Inside a CTA, BW compute
+// warps claim the layer's rows one at a time from a shared counter (in y order forward, reverse
+// order backward) and each publishes its row's progress (points done) in shared memory with
+// st.release.cta after every point.  Before touching point x (and the point it prefetches) a warp
+// checks exactly the rows it reads: the previous row of its own layer (shared memory,
+// ld.acquire.cta = plain LDS) and the two rows of the neighbouring layer (global progress array,
+// relaxed gpu-scope loads, cached in registers and re-polled only when insufficient).  One sync
+// warp per CTA mirrors the shared progress array to global memory behind one st.release.gpu
+// (MEMBAR.GPU, cumulative over what it observed) per round, off the compute path.
+// Polling uses relaxed loads: ld.acquire.gpu / __threadfence emit CCTL.IVALL on sm_100a (whole-L1
+// invalidation) and would wipe the u reuse in L1; a consumer never touches a w line before its
+// producer wrote it, and cross-layer data is read with ld.global.cg after the progress value has
+// returned, so no stale copy can be observed.
 //
 // Forward kernel  = residual f - A u (15-point stencil) + forward L substitution, writes w.
 // Backward kernel = D^{-1} scaling + L^T substitution + u += w, writes w (in place) and u.
@@ -35,11 +34,6 @@
 
 namespace tilu {
 
-// Progress counters are polled with relaxed gpu-scope loads: ld.acquire.gpu would emit
-// CCTL.IVALL (invalidate the SM's whole L1) on every poll and wipe the u-reuse the compute warps
-// rely on.  No acquire is needed for correctness here: a consumer never touches a w line before
-// its producer wrote it (dependency order), so L1 cannot hold a stale copy, and the consumer's
-// data loads are issued only after the flag value has returned (control dependency + bar.sync).
 __device__ __forceinline__ int ld_relaxed(const int *p)
 {
     int v;
@@ -50,134 +44,71 @@ __device__ __forceinline__ void st_release(int *p, int v)
 {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed(int *p, int v)
+{
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta(int *p, int v)
+{
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
 __device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
 
-// Thread 0 waits until the neighbouring layer's progress counter reaches `need`.  A schedule bug
-// must fail loudly, not hang the device: after ~10 s of polling the kernel traps.
-__device__ __forceinline__ void wait_progress(const int *flag, int need)
+// Spin until *flag >= need (flag in shared or global memory).  A dependency bug must fail loudly,
+// not hang the device: after ~10 s of polling the kernel traps.
+__device__ __forceinline__ int wait_shared(const int *flag, int need)
 {
     long long polls = 0;
-    while (ld_relaxed(flag) < need) {
+    int v;
+    while ((v = ld_acquire_cta(flag)) < need) {
+        __nanosleep(32);
+        if (++polls > (1ll << 28)) __trap();
+    }
+    return v;
+}
+__device__ __forceinline__ int wait_global(const int *flag, int need)
+{
+    long long polls = 0;
+    int v;
+    while ((v = ld_relaxed(flag)) < need) {
         __nanosleep(64);
         if (++polls > (1ll << 27)) __trap();
     }
-}
-
-// The sync warp (warp BW) of a CTA: window by window it publishes the CTA's progress (fence +
-// release, after the barrier that closes the window) and makes sure the data the NEXT window
-// reads from the neighbouring layer is published before it arrives at the barrier that opens it.
-// Compute warps only ever meet it at that one barrier per window.
-__device__ __forceinline__ unsigned long long gtimer()
-{
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-// trace layout per CTA (8 x u64): start ns, first-window-open ns, end ns, sync-warp dependency-wait
-// cycles, sync-warp release (MEMBAR) cycles, warp-0 barrier-wait cycles, warp-0 step cycles, windows
-constexpr int TRACE_W = 8;
-
-__device__ __forceinline__ void sync_warp_loop(int *myflag, const int *dep, int depEnd, int D, int t0, int t1,
-                                               unsigned long long *trace)
-{
-    // everything a window starting at tau0 reads from the neighbouring layer (including the PF-ahead
-    // prefetches) has step <= tau0 + BWIN + PF - 2 - D; the neighbour never publishes past depEnd
-    const bool leader = (threadIdx.x & 31) == 0;
-    unsigned long long waited = 0, released = 0, nwin = 0;
-    if (trace && leader) trace[0] = gtimer();
-    if (leader && dep) wait_progress(dep, min(t0 + BWIN + PF - 2 - D, depEnd));
-    if (trace && leader) trace[1] = gtimer();
-    __syncthreads();  // opens the first window
-    for (int tau0 = t0; tau0 <= t1; tau0 += BWIN) {
-        const int tau1 = tau0 + BWIN;
-        if (leader && dep && tau1 <= t1) {
-            const long long a = trace ? clock64() : 0;
-            wait_progress(dep, min(tau1 + BWIN + PF - 2 - D, depEnd));
-            if (trace) waited += clock64() - a;
-        }
-        __syncthreads();  // closes this window / opens the next
-        if (leader) {
-            const long long a = trace ? clock64() : 0;
-            st_release(myflag, min(tau1, t1 + 1) - 1);  // MEMBAR.GPU + store, cumulative over the barrier
-            if (trace) released += clock64() - a;
-        }
-        ++nwin;
-    }
-    if (trace && leader) {
-        trace[2] = gtimer();
-        trace[3] = waited;
-        trace[4] = released;
-        trace[7] = nwin;
-    }
+    return v;
 }
 
 __device__ __forceinline__ bool in_band_b(int x, int y, int z, int xe) { return z == 1 || y == 1 || x == 1 || x == xe; }
-__device__ __forceinline__ int band_idx_b(const PlanDev &P, int row, int x, int y, int z)
-{
-    return P.bandoff[row] + ((z == 1 || y == 1) ? x - 1 : (x == 1 ? 0 : 1));
-}
 
-__device__ __forceinline__ double lq_b(const PlanDev &P, int m, int qx, int qy, int qz, double dval)
+// Sync warp: mirror this layer's per-row progress (shared) to the global array the neighbouring
+// layer polls.  Each round: read all rows, one st.release.gpu (MEMBAR.GPU, cumulative over the
+// observed progress and thus over the w stores it covers), then relaxed stores of the values.
+__device__ __forceinline__ void progress_mirror(const int *s_prog, const int *s_done, int *gp, int R, int lane)
 {
-    const int n = P.n;
-    if (!interior(qx, qy, qz, n)) return 0.0;
-    if (P.variant == 1) {
-        const int xe = n - 1 - qz - qy;
-        if (in_band_b(qx, qy, qz, xe)) return P.store[9 * (int64_t)band_idx_b(P, row_id(n, qz, qy), qx, qy, qz) + m];
-    }
-    return dval;
-}
-
-// ----------------------------------------------------------------------------------------------
-// host: greedy list schedule
-// ----------------------------------------------------------------------------------------------
-void batch_schedule(int n, int bwin, int pf, std::vector<LayerSched> &layers, std::vector<RowSched> &rows, int &Tmax,
-                    int &D)
-{
-    const int nl = n - 3;
-    const int amin = bwin + 1 + pf;
-    D = 2 * bwin + 1 + pf;
-    layers.assign(nl, LayerSched{});
-    rows.assign((size_t)(n - 3) * (n - 2) / 2 + 1, RowSched{0, 0, 0});
-    Tmax = 0;
-    for (int z = 1; z <= nl; ++z) {
-        const int R = n - 2 - z;
-        LayerSched &L = layers[z - 1];
-        int free_at[BW], lastrow[BW];
-        for (int w = 0; w < BW; ++w) {
-            free_at[w] = 0;
-            lastrow[w] = 0;
-            L.first[w] = L.last[w] = 0;
+    constexpr int PER = (MAXR + 31) / 32;
+    for (;;) {
+        const int done = ld_acquire_cta(s_done);
+        int v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int y = lane + 1 + 32 * k;
+            v[k] = y <= R ? ld_acquire_cta(&s_prog[y]) : 0;
         }
-        int prev_start = -(1 << 29);
-        L.T0 = 1 << 30;
-        L.T1 = 0;
-        for (int y = 1; y <= R; ++y) {
-            const int m = n - 1 - z - y;
-            int t = std::max(0, prev_start + amin);
-            if (z > 1) {
-                t = std::max(t, rows[row_id(n, z - 1, y + 1)].start + 1 + D);
-                t = std::max(t, rows[row_id(n, z - 1, y)].start + 2 + D);
-            }
-            int wbest = 0;
-            for (int w = 1; w < BW; ++w)
-                if (free_at[w] < free_at[wbest]) wbest = w;
-            t = std::max(t, free_at[wbest]);
-            RowSched &rs = rows[row_id(n, z, y)];
-            rs.start = t;
-            rs.next = 0;
-            rs.prev = lastrow[wbest];
-            if (lastrow[wbest]) rows[row_id(n, z, lastrow[wbest])].next = y;
-            else L.first[wbest] = y;
-            lastrow[wbest] = y;
-            L.last[wbest] = y;
-            free_at[wbest] = t + m;
-            prev_start = t;
-            L.T0 = std::min(L.T0, t);
-            L.T1 = std::max(L.T1, t + m - 1);
+        __syncwarp();
+        if (lane == 0) st_release(&gp[MAXR + 2], done);  // the MEMBAR.GPU of this round
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int y = lane + 1 + 32 * k;
+            if (y <= R) st_relaxed(&gp[y], v[k]);
         }
-        Tmax = std::max(Tmax, L.T1);
+        if (done >= R) return;  // `done` was read before the values: they are final
+        __nanosleep(256);
     }
 }
 
@@ -199,9 +130,6 @@ __device__ __forceinline__ void smem_load_table(double *tab, const double *__res
 template <int M, int K>
 __device__ __forceinline__ void smem_march(double *tab, int lane)
 {
-#ifdef TILU_ABLATE_NOMARCH
-    return;
-#endif
     constexpr int NE = M * (K - 1);
     if (NE == 0) return;
     constexpr int IT = NE > 0 ? (NE + 31) / 32 : 1;
@@ -228,36 +156,20 @@ __device__ __forceinline__ void smem_march(double *tab, int lane)
 
 // ----------------------------------------------------------------------------------------------
 // forward: residual + L solve
-//
-// Per compute warp: one row at a time.  Loads run PF points ahead through a RING-slot register
-// ring; the window loop is unrolled RING (= BWIN) times so every ring index is a compile-time
-// constant: the point processed at step tau uses slot (tau - T0) % RING, the prefetch issued at
-// tau fills slot (tau + PF - T0) % RING.
 // ----------------------------------------------------------------------------------------------
 struct FwdSlot {
     double ue, us, un, ubn, ubc, uts, utc, f, ws, wbn, wbc;
 };
 
 struct FwdRow {
-    int y, m, rid, start;
-    int boff;           // first band-store entry of the row (V1)
+    int y, m, rid, boff;
     uint32_t oc, os, on, obn, obc, ots, otc;
-    double lring[RING];  // lane m < 7: prefetched band-store entry L_m of the slot's point (V1)
-    // sliding windows: the values of point x-1 / x that point x+1 reuses
-    double u_wm, u_c, us0, un_m, ubn_m, ubc0, uts0, utc_m, ws0, wbn_m, wbc0, wprev;
-    FwdSlot ring[RING];
-    double ss;
 };
 
 __device__ __forceinline__ void fwd_load(FwdSlot &S, const double *__restrict__ u, const double *__restrict__ f,
                                          const double *__restrict__ w, const FwdRow &R, int p)
 {
     const uint32_t X = (uint32_t)p * 32u;
-#ifdef TILU_ABLATE_NOLOAD
-    S.ue = X * 1e-9; S.us = S.ue + 1; S.un = S.ue + 2; S.ubn = S.ue + 3; S.ubc = S.ue + 4; S.uts = S.ue + 5;
-    S.utc = S.ue + 6; S.f = S.ue + 7; S.ws = S.ue + 8; S.wbn = S.ue + 9; S.wbc = S.ue + 10;
-    return;
-#endif
     S.ue = u[R.oc + X + 32];
     S.us = u[R.os + X + 32];
     S.un = u[R.on + X];
@@ -266,12 +178,12 @@ __device__ __forceinline__ void fwd_load(FwdSlot &S, const double *__restrict__ 
     S.uts = u[R.ots + X + 32];
     S.utc = u[R.otc + X];
     S.f = f[R.oc + X];
-    S.ws = ldcg(w + R.os + X + 32);
-    S.wbn = ldcg(w + R.obn + X);
+    S.ws = w[R.os + X + 32];          // same layer: written by a warp of this CTA
+    S.wbn = ldcg(w + R.obn + X);      // layer below: written by another CTA
     S.wbc = ldcg(w + R.obc + X + 32);
 }
 
-// Lane m < 7 fetches the V1 band-store entry L_m of point p (uniform over the warp's tets) ahead.
+// Lane m < 7 fetches the V1 band-store entry L_m of point p (uniform over the warp's tets).
 __device__ __forceinline__ void fwd_band_load(double &dst, const PlanDev &P, const FwdRow &R, int z, int p, int lane)
 {
     if (P.variant == 1 && lane < 7 && in_band_b(p, R.y, z, R.m))
@@ -281,75 +193,78 @@ __device__ __forceinline__ void fwd_band_load(double &dst, const PlanDev &P, con
 template <int K, bool EXACT, bool CONST_ROW>
 __global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
 {
-    // Rolled step loop with a current / next load buffer (one point of prefetch): smaller code and
-    // register footprint than the unrolled ring, which lets two CTAs (18 warps) share an SM.
-    __shared__ int s_ticket;
+    __shared__ int s_ticket, s_next, s_done;
+    __shared__ int s_prog[MAXR + 2];
     __shared__ double s_red[BW][32];
     __shared__ double s_tab[BW][7 * K];
     __shared__ double s_L[BW][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(A.ticket, 1) + 1;  // counter starts at -1
+    if (threadIdx.x == 0) {
+        s_ticket = atomicAdd(A.ticket, 1);
+        s_next = 0;
+        s_done = 0;
+    }
+    for (int i = threadIdx.x; i < MAXR + 2; i += NT) s_prog[i] = i == 0 ? (1 << 30) : 0;  // row 0: boundary
     __syncthreads();
     if (A.max_ticket >= 0 && s_ticket > A.max_ticket) return;
-    const int nl = P.n - 3;
+    const int nl = P.n - 3, n = P.n;
     const int zi = s_ticket / A.G, g = s_ticket - (s_ticket / A.G) * A.G;
-    const int n = P.n, z = zi + 1;
-    const int T0 = A.sched[zi].T0, T1 = A.sched[zi].T1;
-    int *myflag = A.flags + g * nl + zi;
+    const int z = zi + 1, Rn = n - 2 - z;
+    int *gp = A.gprog + ((size_t)g * nl + zi) * GSTRIDE;
+    const int *gb = z > 1 ? gp - GSTRIDE : nullptr;  // layer below
+    double ss = 0.0;
     if (warp == BW) {
-        sync_warp_loop(myflag, z > 1 ? myflag - 1 : nullptr, z > 1 ? A.sched[zi - 1].T1 : 0, A.D, T0, T1,
-                       A.trace ? A.trace + TRACE_W * (size_t)s_ticket : nullptr);
+        progress_mirror(s_prog, &s_done, gp, Rn, lane);
     } else {
-        const size_t gb = (size_t)g * P.grid * 32 + lane;
-        const double *__restrict__ u = A.u + gb;
-        const double *__restrict__ f = A.f + gb;
-        double *__restrict__ w = A.w + gb;
+        const size_t gbase = (size_t)g * P.grid * 32 + lane;
+        const double *__restrict__ u = A.u + gbase;
+        const double *__restrict__ f = A.f + gbase;
+        double *__restrict__ w = A.w + gbase;
         double *tab = s_tab[warp];
         double *sL = s_L[warp];
-        FwdRow R;
-        R.y = A.sched[zi].first[warp];
-        R.start = R.y ? A.rows[row_id(n, z, R.y)].start : 0;
-        R.ss = 0.0;
-        FwdSlot C{}, N{};
-        double cband = 0.0, nband = 0.0;
-        __syncthreads();  // first window opened by the sync warp
-        for (int tau0 = T0; tau0 <= T1; tau0 += BWIN) {
-            for (int tau = tau0; tau < tau0 + BWIN; ++tau) {
-                if (!R.y) break;
-                const int x = tau - R.start + 1;
-                if (x < 1) continue;
-                if (x == 1) {  // row start: offsets, seed table, windows, point-1 values
-                    const int y = R.y;
-                    R.m = n - 1 - z - y;
-                    R.rid = row_id(n, z, y);
-                    R.oc = (uint32_t)row_offset(n, z, y) * 32u;
-                    R.os = (uint32_t)row_offset(n, z, y - 1) * 32u;
-                    R.on = (uint32_t)row_offset(n, z, y + 1) * 32u;
-                    R.obn = (uint32_t)row_offset(n, z - 1, y + 1) * 32u;
-                    R.obc = (uint32_t)row_offset(n, z - 1, y) * 32u;
-                    R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
-                    R.otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
-                    R.boff = P.variant == 1 ? P.bandoff[R.rid] : 0;
-                    smem_load_table<7, K>(tab, P.seedF + (int64_t)R.rid * 7 * K, lane);
-                    R.u_wm = u[R.oc];
-                    R.u_c = u[R.oc + 32];
-                    R.us0 = u[R.os + 32];
-                    R.un_m = u[R.on];
-                    R.ubn_m = u[R.obn];
-                    R.ubc0 = u[R.obc + 32];
-                    R.uts0 = u[R.ots + 32];
-                    R.utc_m = u[R.otc];
-                    R.ws0 = ldcg(w + R.os + 32);
-                    R.wbn_m = ldcg(w + R.obn);
-                    R.wbc0 = ldcg(w + R.obc + 32);
-                    R.wprev = 0.0;
-                    fwd_load(C, u, f, w, R, 1);
-                    fwd_band_load(cband, P, R, z, 1, lane);
+        for (;;) {
+            int y = 0;
+            if (lane == 0) y = atomicAdd(&s_next, 1) + 1;
+            y = __shfl_sync(0xffffffffu, y, 0);
+            if (y > Rn) break;
+            FwdRow R;
+            R.y = y;
+            R.m = n - 1 - z - y;
+            R.rid = row_id(n, z, y);
+            R.oc = (uint32_t)row_offset(n, z, y) * 32u;
+            R.os = (uint32_t)row_offset(n, z, y - 1) * 32u;
+            R.on = (uint32_t)row_offset(n, z, y + 1) * 32u;
+            R.obn = (uint32_t)row_offset(n, z - 1, y + 1) * 32u;
+            R.obc = (uint32_t)row_offset(n, z - 1, y) * 32u;
+            R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
+            R.otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
+            R.boff = P.variant == 1 ? P.bandoff[R.rid] : 0;
+            const int m = R.m;
+            smem_load_table<7, K>(tab, P.seedF + (int64_t)R.rid * 7 * K, lane);
+            // dependencies of point p: row y-1 of this layer (length m+1) up to p+1; the layer
+            // below: row y (length m+1) up to p+1 and row y+1 (length m) up to p
+            int cs = 0, cby = 0, cbn = 0;
+            auto ensure = [&](int p) {
+                if (cs < p + 1) cs = wait_shared(&s_prog[y - 1], p + 1);
+                if (gb) {
+                    if (cby < p + 1) cby = wait_global(&gb[y], p + 1);
+                    if (cbn < p) cbn = wait_global(&gb[y + 1], p);
                 }
-                // prefetch point x+1 (branch-free: at the row end it re-reads point m, unused)
-                const int pp = min(x + 1, R.m);
-                fwd_load(N, u, f, w, R, pp);
-                fwd_band_load(nband, P, R, z, pp, lane);
+            };
+            ensure(1);
+            // sliding windows (values of point x-1 / x that point x+1 reuses) and point 1
+            double u_wm = u[R.oc], u_c = u[R.oc + 32], us0 = u[R.os + 32], un_m = u[R.on], ubn_m = u[R.obn];
+            double ubc0 = u[R.obc + 32], uts0 = u[R.ots + 32], utc_m = u[R.otc];
+            double ws0 = w[R.os + 32], wbn_m = ldcg(w + R.obn), wbc0 = ldcg(w + R.obc + 32), wprev = 0.0;
+            FwdSlot C, N;
+            fwd_load(C, u, f, w, R, 1);
+            double cband = 0.0, nband = 0.0;
+            fwd_band_load(cband, P, R, z, 1, lane);
+            for (int x = 1; x <= m; ++x) {
+                const int pn = min(x + 1, m);  // prefetch (at the row end: re-read point m, unused)
+                ensure(pn);
+                fwd_load(N, u, f, w, R, pn);
+                fwd_band_load(nband, P, R, z, pn, lane);
                 double ap[15];
                 const double *a = A.arow;
                 if (!CONST_ROW) {
@@ -359,70 +274,67 @@ __global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
                     a = ap;
                 }
                 // residual in stencil_apply order (_kernels.py:255-266), then f - A u
-                double acc = EXACT ? dmul(a[7], R.u_c) : a[7] * R.u_c;
-                acc = madd<EXACT>(acc, a[0], R.u_wm);
-                acc = madd<EXACT>(acc, a[1], R.us0);
+                double acc = EXACT ? dmul(a[7], u_c) : a[7] * u_c;
+                acc = madd<EXACT>(acc, a[0], u_wm);
+                acc = madd<EXACT>(acc, a[1], us0);
                 acc = madd<EXACT>(acc, a[2], C.us);
-                acc = madd<EXACT>(acc, a[3], R.ubn_m);
+                acc = madd<EXACT>(acc, a[3], ubn_m);
                 acc = madd<EXACT>(acc, a[4], C.ubn);
-                acc = madd<EXACT>(acc, a[5], R.ubc0);
+                acc = madd<EXACT>(acc, a[5], ubc0);
                 acc = madd<EXACT>(acc, a[6], C.ubc);
                 acc = madd<EXACT>(acc, a[8], C.ue);
                 acc = madd<EXACT>(acc, a[9], C.un);
-                acc = madd<EXACT>(acc, a[10], R.un_m);
+                acc = madd<EXACT>(acc, a[10], un_m);
                 acc = madd<EXACT>(acc, a[11], C.uts);
-                acc = madd<EXACT>(acc, a[12], R.uts0);
+                acc = madd<EXACT>(acc, a[12], uts0);
                 acc = madd<EXACT>(acc, a[13], C.utc);
-                acc = madd<EXACT>(acc, a[14], R.utc_m);
+                acc = madd<EXACT>(acc, a[14], utc_m);
                 const double r = dsub(C.f, acc);
-                R.ss = fma(r, r, R.ss);
+                ss = fma(r, r, ss);
                 // L entries: lane m publishes L_m (band store or the shared NDDF table)
-                if (lane < 7) sL[lane] = (P.variant == 1 && in_band_b(x, R.y, z, R.m)) ? cband : tab[lane * K];
+                if (lane < 7) sL[lane] = (P.variant == 1 && in_band_b(x, y, z, m)) ? cband : tab[lane * K];
                 __syncwarp();
                 double v;
                 if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
-                    v = msub<true>(r, sL[0], R.wprev);
-                    v = msub<true>(v, sL[1], R.ws0);
+                    v = msub<true>(r, sL[0], wprev);
+                    v = msub<true>(v, sL[1], ws0);
                     v = msub<true>(v, sL[2], C.ws);
-                    v = msub<true>(v, sL[3], R.wbn_m);
+                    v = msub<true>(v, sL[3], wbn_m);
                     v = msub<true>(v, sL[4], C.wbn);
-                    v = msub<true>(v, sL[5], R.wbc0);
+                    v = msub<true>(v, sL[5], wbc0);
                     v = msub<true>(v, sL[6], C.wbc);
                 } else {  // own-row term last: one FMA on the row's dependency chain
-                    v = msub<false>(r, sL[1], R.ws0);
+                    v = msub<false>(r, sL[1], ws0);
                     v = msub<false>(v, sL[2], C.ws);
-                    v = msub<false>(v, sL[3], R.wbn_m);
+                    v = msub<false>(v, sL[3], wbn_m);
                     v = msub<false>(v, sL[4], C.wbn);
-                    v = msub<false>(v, sL[5], R.wbc0);
+                    v = msub<false>(v, sL[5], wbc0);
                     v = msub<false>(v, sL[6], C.wbc);
-                    v = msub<false>(v, sL[0], R.wprev);
+                    v = msub<false>(v, sL[0], wprev);
                 }
                 w[R.oc + (uint32_t)x * 32u] = v;
-                smem_march<7, K>(tab, lane);
-                R.u_wm = R.u_c;
-                R.u_c = C.ue;
-                R.us0 = C.us;
-                R.un_m = C.un;
-                R.ubn_m = C.ubn;
-                R.ubc0 = C.ubc;
-                R.uts0 = C.uts;
-                R.utc_m = C.utc;
-                R.ws0 = C.ws;
-                R.wbn_m = C.wbn;
-                R.wbc0 = C.wbc;
-                R.wprev = v;
+                smem_march<7, K>(tab, lane);  // ends with __syncwarp: orders this point's stores
+                if (lane == 0) st_release_cta(&s_prog[y], x);
+                u_wm = u_c;
+                u_c = C.ue;
+                us0 = C.us;
+                un_m = C.un;
+                ubn_m = C.ubn;
+                ubc0 = C.ubc;
+                uts0 = C.uts;
+                utc_m = C.utc;
+                ws0 = C.ws;
+                wbn_m = C.wbn;
+                wbc0 = C.wbc;
+                wprev = v;
                 C = N;
                 cband = nband;
-                if (x == R.m) {
-                    R.y = A.rows[R.rid].next;
-                    if (R.y) R.start = A.rows[row_id(n, z, R.y)].start;
-                }
             }
-            __syncthreads();
+            if (lane == 0) atomicAdd(&s_done, 1);
         }
-        s_red[warp][lane] = R.ss;
     }
     if (A.part) {
+        if (warp < BW) s_red[warp][lane] = ss;
         __syncthreads();
         if (warp == 0) {
             double t = 0.0;
@@ -434,70 +346,101 @@ __global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
 }
 
 // ----------------------------------------------------------------------------------------------
-// backward: D^{-1} + L^T solve + update, exact time reversal of the forward schedule
+// backward: D^{-1} + L^T solve + update (rows in descending y, points in descending x)
 // ----------------------------------------------------------------------------------------------
 struct BwdSlot {
     double wn, wts, wtc, wf, u;
 };
 
 struct BwdRow {
-    int y, m, rid, bstart;  // bstart: backward step of the row's first point (x = m)
-    int qboff, qrow_band, qxe;  // lane m < 7: band offset / band-row flag / length of the row of q_m = p - d_m;
-                                // lane 7: the own row (1/D)
+    int y, m, rid;
+    int qboff, qrow_band, qxe;  // lane m < 7: band offset / band-row flag / length of the row of
+                                // q_m = p - d_m; lane 7: the own row (1/D)
     uint32_t oc, on, ots, otc;
-    double lring[RING];   // lane m: prefetched value of L_m at q_m (lane 7: 1/D at p)
-    unsigned lsrc;        // 2 bits per slot: 0 = q outside the interior, 1 = band store, 2 = NDDF
-    double wn_hi, wts_hi, wtc_hi, wprev;
-    BwdSlot ring[RING];
 };
 
 __device__ __forceinline__ void bwd_load(BwdSlot &S, const double *__restrict__ u, const double *__restrict__ w,
                                          const BwdRow &R, int x)
 {
     const uint32_t X = (uint32_t)x * 32u;
-    S.wn = ldcg(w + R.on + X - 32);
-    S.wts = ldcg(w + R.ots + X);
+    S.wn = w[R.on + X - 32];         // same layer (row y+1): written by a warp of this CTA
+    S.wts = ldcg(w + R.ots + X);     // layer above: written by another CTA
     S.wtc = ldcg(w + R.otc + X - 32);
     S.wf = w[R.oc + X];
     S.u = u[R.oc + X];
 }
 
-// Lane m < 7 classifies q_m = p - d_m of point (x, y, z) and fetches its band-store entry L_m ahead
-// (_kernels.py:434-441 _lq); lane 7 does the same for 1/D at p.  Result: source code in R.lsrc.
-__device__ __forceinline__ void bwd_band_load(BwdRow &R, const PlanDev &P, int n, int z, int x, int lane, int SLOT)
+// Lane m < 7 classifies q_m = p - d_m of point (x, y, z) and fetches its band-store entry L_m
+// (_kernels.py:434-441 _lq); lane 7 does the same for 1/D at p.  Returns the source code:
+// 0 = q outside the interior, 1 = band store (value in dst), 2 = NDDF table.
+__device__ __forceinline__ int bwd_band_load(double &dst, const BwdRow &R, const PlanDev &P, int n, int z, int x,
+                                             int lane)
 {
-    if (lane >= 8) return;
-    unsigned code = 2;
+    if (lane >= 8) return 2;
     if (lane < 7) {
         const int qx = x - kDX[lane], qy = R.y - kDY[lane], qz = z - kDZ[lane];
-        if (!interior(qx, qy, qz, n)) code = 0;
-        else if (P.variant == 1 && (R.qrow_band || qx == 1 || qx == R.qxe)) {
-            code = 1;
-            R.lring[SLOT] = P.store[9 * (int64_t)(R.qboff + (R.qrow_band ? qx - 1 : (qx == 1 ? 0 : 1))) + lane];
+        if (!interior(qx, qy, qz, n)) return 0;
+        if (P.variant == 1 && (R.qrow_band || qx == 1 || qx == R.qxe)) {
+            dst = P.store[9 * (int64_t)(R.qboff + (R.qrow_band ? qx - 1 : (qx == 1 ? 0 : 1))) + lane];
+            return 1;
         }
-    } else if (P.variant == 1 && in_band_b(x, R.y, z, R.m)) {
-        code = 1;
-        R.lring[SLOT] = P.store[9 * (int64_t)(R.qboff + ((z == 1 || R.y == 1) ? x - 1 : (x == 1 ? 0 : 1))) + 8];
+        return 2;
     }
-    R.lsrc = (R.lsrc & ~(3u << (2 * SLOT))) | (code << (2 * SLOT));
+    if (P.variant == 1 && in_band_b(x, R.y, z, R.m)) {
+        dst = P.store[9 * (int64_t)(R.qboff + ((z == 1 || R.y == 1) ? x - 1 : (x == 1 ? 0 : 1))) + 8];
+        return 1;
+    }
+    return 2;
 }
 
-template <int K, bool EXACT, int SLOT>
-__device__ __forceinline__ void bwd_step(BwdRow &R, const PlanDev &P, const BatchArgs &A, int n, int z, int tau,
-                                         double *__restrict__ u, double *__restrict__ w, double *tab, double *sL,
-                                         int lane)
+template <int K, bool EXACT>
+__global__ void __launch_bounds__(NT, 2) k_batch_bwd(PlanDev P, BatchArgs A)
 {
-    if (!R.y) return;
-    const int k = tau - R.bstart;  // 0-based position along the descending row
-    if (k < 0) return;
-    const int y = R.y;
-    if (k == 0) {
+    __shared__ int s_ticket, s_next, s_done;
+    __shared__ int s_prog[MAXR + 2];
+    __shared__ double s_tab[BW][8 * K];
+    __shared__ double s_L[BW][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        s_ticket = atomicAdd(A.ticket, 1);
+        s_next = 0;
+        s_done = 0;
+    }
+    for (int i = threadIdx.x; i < MAXR + 2; i += NT) s_prog[i] = 0;
+    __syncthreads();
+    if (A.max_ticket >= 0 && s_ticket > A.max_ticket) return;
+    const int nl = P.n - 3, n = P.n;
+    const int li = s_ticket / A.G, g = s_ticket - li * A.G;
+    const int zi = nl - 1 - li;
+    const int z = zi + 1, Rn = n - 2 - z;
+    if (threadIdx.x == 0) s_prog[Rn + 1] = 1 << 30;  // row R+1 of this layer: boundary
+    __syncthreads();
+    int *gp = A.gprog + ((size_t)g * nl + zi) * GSTRIDE;
+    const int *ga = z < nl ? gp + GSTRIDE : nullptr;  // layer above
+    if (warp == BW) {
+        progress_mirror(s_prog, &s_done, gp, Rn, lane);
+        return;
+    }
+    const size_t gbase = (size_t)g * P.grid * 32 + lane;
+    double *__restrict__ u = A.u + gbase;
+    double *__restrict__ w = A.w + gbase;
+    double *tab = s_tab[warp];
+    double *sL = s_L[warp];
+    for (;;) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(&s_next, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        const int y = Rn - t;
+        if (y < 1) break;
+        BwdRow R;
+        R.y = y;
         R.m = n - 1 - z - y;
         R.rid = row_id(n, z, y);
         R.oc = (uint32_t)row_offset(n, z, y) * 32u;
         R.on = (uint32_t)row_offset(n, z, y + 1) * 32u;
         R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
         R.otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
+        const int m = R.m;
         if (lane < 8) {  // the row of q_m (lane m) or the own row (lane 7)
             const int qy = lane < 7 ? y - kDY[lane] : y, qz = lane < 7 ? z - kDZ[lane] : z;
             const bool valid = qy >= 1 && qz >= 1 && qy + qz <= n - 2;
@@ -506,101 +449,67 @@ __device__ __forceinline__ void bwd_step(BwdRow &R, const PlanDev &P, const Batc
             R.qboff = (P.variant == 1 && valid) ? P.bandoff[row_id(n, qz, qy)] : 0;
         }
         smem_load_table<8, K>(tab, P.seedB + (int64_t)R.rid * 8 * K, lane);
-        const uint32_t M = (uint32_t)R.m * 32u;
-        R.wn_hi = ldcg(w + R.on + M);
-        R.wts_hi = ldcg(w + R.ots + M + 32);
-        R.wtc_hi = ldcg(w + R.otc + M);
-        R.wprev = 0.0;
-#pragma unroll
-        for (int q = 0; q < PF; ++q)
-            if (R.m - q >= 1) {
-                bwd_load(R.ring[(SLOT + q) % RING], u, w, R, R.m - q);
-                bwd_band_load(R, P, n, z, R.m - q, lane, (SLOT + q) % RING);
+        // dependencies of the k-th point (x = m - k + 1): row y+1 of this layer (length m-1) and
+        // row y of the layer above (length m-1) up to min(k, m-1) points, row y-1 of the layer above
+        // (length m) up to k points
+        int cn = 0, cts = 0, ctc = 0;
+        auto ensure = [&](int k) {
+            const int k1 = min(k, m - 1);
+            if (cn < k1) cn = wait_shared(&s_prog[y + 1], k1);
+            if (ga) {
+                if (y >= 2 && cts < k) cts = wait_global(&ga[y - 1], k);
+                if (y <= Rn - 1 && ctc < k1) ctc = wait_global(&ga[y], k1);
             }
-    }
-    const int x = R.m - k;
-    const BwdSlot C = R.ring[SLOT];
-    if (lane < 8) {
-        const unsigned code = (R.lsrc >> (2 * SLOT)) & 3u;
-        sL[lane] = code == 0 ? 0.0 : (code == 1 ? R.lring[SLOT] : tab[lane * K]);
-    }
-    __syncwarp();
-    double Lq[7];
-#pragma unroll
-    for (int mm = 0; mm < 7; ++mm) Lq[mm] = sL[mm];
-    const double inv_d = sL[7];
-    double v = EXACT ? dmul(inv_d, C.wf) : inv_d * C.wf;
-    if (EXACT) {  // reference order (_kernels.py:404-425)
-        v = msub<true>(v, Lq[0], R.wprev);
-        v = msub<true>(v, Lq[1], R.wn_hi);
-        v = msub<true>(v, Lq[2], C.wn);
-        v = msub<true>(v, Lq[3], R.wts_hi);
-        v = msub<true>(v, Lq[4], C.wts);
-        v = msub<true>(v, Lq[5], R.wtc_hi);
-        v = msub<true>(v, Lq[6], C.wtc);
-    } else {
-        v = msub<false>(v, Lq[1], R.wn_hi);
-        v = msub<false>(v, Lq[2], C.wn);
-        v = msub<false>(v, Lq[3], R.wts_hi);
-        v = msub<false>(v, Lq[4], C.wts);
-        v = msub<false>(v, Lq[5], R.wtc_hi);
-        v = msub<false>(v, Lq[6], C.wtc);
-        v = msub<false>(v, Lq[0], R.wprev);
-    }
-    const uint32_t X = (uint32_t)x * 32u;
-    w[R.oc + X] = v;
-    u[R.oc + X] = dadd(C.u, v);
-    {   // prefetch point x-PF (branch-free: below x = 1 the loads re-read point 1, unused)
-        const int pp = max(x - PF, 1);
-        bwd_load(R.ring[(SLOT + PF) % RING], u, w, R, pp);
-        bwd_band_load(R, P, n, z, pp, lane, (SLOT + PF) % RING);
-    }
-    smem_march<8, K>(tab, lane);
-    R.wn_hi = C.wn;
-    R.wts_hi = C.wts;
-    R.wtc_hi = C.wtc;
-    R.wprev = v;
-    if (x == 1) {
-        R.y = A.rows[R.rid].prev;
-        if (R.y) R.bstart = A.Tmax - (A.rows[row_id(n, z, R.y)].start + (n - 1 - z - R.y) - 1);
-    }
-}
-
-template <int K, bool EXACT>
-__global__ void __launch_bounds__(NT, 2) k_batch_bwd(PlanDev P, BatchArgs A)
-{
-    __shared__ int s_ticket;
-    __shared__ double s_tab[BW][8 * K];
-    __shared__ double s_L[BW][8];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(A.ticket, 1) + 1;
-    __syncthreads();
-    const int nl = P.n - 3;
-    const int li = s_ticket / A.G, g = s_ticket - li * A.G;
-    const int zi = nl - 1 - li;
-    const int n = P.n, z = zi + 1;
-    int *myflag = A.flags + g * nl + zi;
-    const int tb0 = A.Tmax - A.sched[zi].T1, tb1 = A.Tmax - A.sched[zi].T0;
-    if (warp == BW) {
-        sync_warp_loop(myflag, z < nl ? myflag + 1 : nullptr, z < nl ? A.Tmax - A.sched[zi + 1].T0 : 0, A.D, tb0,
-                       tb1, A.trace ? A.trace + TRACE_W * (size_t)s_ticket : nullptr);
-        return;
-    }
-    const size_t gb = (size_t)g * P.grid * 32 + lane;
-    double *__restrict__ u = A.u + gb;
-    double *__restrict__ w = A.w + gb;
-    double *tab = s_tab[warp];
-    BwdRow R;
-    R.lsrc = 0;
-    R.y = A.sched[zi].last[warp];
-    R.bstart = R.y ? A.Tmax - (A.rows[row_id(n, z, R.y)].start + (n - 1 - z - R.y) - 1) : 0;
-    __syncthreads();  // first window opened by the sync warp
-    for (int tau0 = tb0; tau0 <= tb1; tau0 += BWIN) {
-        bwd_step<K, EXACT, 0>(R, P, A, n, z, tau0 + 0, u, w, tab, s_L[warp], lane);
-        bwd_step<K, EXACT, 1>(R, P, A, n, z, tau0 + 1, u, w, tab, s_L[warp], lane);
-        bwd_step<K, EXACT, 2>(R, P, A, n, z, tau0 + 2, u, w, tab, s_L[warp], lane);
-        bwd_step<K, EXACT, 3>(R, P, A, n, z, tau0 + 3, u, w, tab, s_L[warp], lane);
-        __syncthreads();
+        };
+        ensure(1);
+        const uint32_t M = (uint32_t)m * 32u;
+        double wn_hi = w[R.on + M], wts_hi = ldcg(w + R.ots + M + 32), wtc_hi = ldcg(w + R.otc + M), wprev = 0.0;
+        BwdSlot C, N;
+        bwd_load(C, u, w, R, m);
+        double cband = 0.0, nband = 0.0;
+        int csrc = bwd_band_load(cband, R, P, n, z, m, lane), nsrc = 2;
+        for (int k = 1; k <= m; ++k) {
+            const int x = m - k + 1;
+            const int kn = min(k + 1, m);  // prefetch the next point (at the row end: re-read x = 1)
+            ensure(kn);
+            const int xn = m - kn + 1;
+            bwd_load(N, u, w, R, xn);
+            nsrc = bwd_band_load(nband, R, P, n, z, xn, lane);
+            if (lane < 8) sL[lane] = csrc == 0 ? 0.0 : (csrc == 1 ? cband : tab[lane * K]);
+            __syncwarp();
+            const double inv_d = sL[7];
+            double v = EXACT ? dmul(inv_d, C.wf) : inv_d * C.wf;
+            if (EXACT) {  // reference order (_kernels.py:404-425)
+                v = msub<true>(v, sL[0], wprev);
+                v = msub<true>(v, sL[1], wn_hi);
+                v = msub<true>(v, sL[2], C.wn);
+                v = msub<true>(v, sL[3], wts_hi);
+                v = msub<true>(v, sL[4], C.wts);
+                v = msub<true>(v, sL[5], wtc_hi);
+                v = msub<true>(v, sL[6], C.wtc);
+            } else {
+                v = msub<false>(v, sL[1], wn_hi);
+                v = msub<false>(v, sL[2], C.wn);
+                v = msub<false>(v, sL[3], wts_hi);
+                v = msub<false>(v, sL[4], C.wts);
+                v = msub<false>(v, sL[5], wtc_hi);
+                v = msub<false>(v, sL[6], C.wtc);
+                v = msub<false>(v, sL[0], wprev);
+            }
+            const uint32_t X = (uint32_t)x * 32u;
+            w[R.oc + X] = v;
+            u[R.oc + X] = dadd(C.u, v);
+            smem_march<8, K>(tab, lane);  // ends with __syncwarp: orders this point's stores
+            if (lane == 0) st_release_cta(&s_prog[y], k);
+            wn_hi = C.wn;
+            wts_hi = C.wts;
+            wtc_hi = C.wtc;
+            wprev = v;
+            C = N;
+            cband = nband;
+            csrc = nsrc;
+        }
+        if (lane == 0) atomicAdd(&s_done, 1);
     }
 }
 

@@ -38,10 +38,7 @@ struct PlanDev {
 
 struct tilu_plan {
     tilu::PlanDev dev;
-    // batched (packed) path schedule
-    const void *bsched;  // device LayerSched[n-3]
-    const void *brows;   // device RowSched[nrows]
-    int bTmax, bD;
+    const void *bsched;  // non-null: the batched (packed) path supports this level
     double harow[15];  // host copy of the constant stencil (batched kernel parameters)
     int flags;
     int64_t interior;

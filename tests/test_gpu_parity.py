@@ -303,3 +303,22 @@ def test_macro_mesh_smoother_resident_equals_apply():
     mm.store(u2)
     assert torch.equal(u1, u2)
     torch.testing.assert_close(n1, n2, rtol=1e-12, atol=0)
+
+
+def test_packed_dataflow_repeatable_and_equals_simple():
+    """The dataflow kernels' inter-warp / inter-CTA handoffs leave no room for races: repeated
+    runs are bitwise identical and equal the one-CTA-per-tet reference-layout kernels."""
+    level, q, T = 6, 5, 70
+    src, fit, u0 = _oracle_case(level, q, verts=lattice.kuhn_tet((0, 2, 1)))
+    rng = np.random.default_rng(9)
+    us = cuda(np.stack([u0 * s for s in rng.uniform(-1, 1, T)]))
+    fs = cuda(np.zeros((T, len(u0))))
+    fast = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data)
+    simple = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data,
+                        simple=True)
+    ref = us.clone()
+    simple.sweep(ref, fs, 3)
+    for _ in range(3):
+        got = us.clone()
+        fast.sweep(got, fs, 3)
+        assert torch.equal(got, ref)
