@@ -320,6 +320,7 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
             return fail(TILU_EINVAL, "band_ranks is not the canonical boundary band of level %d", d->level);
         }
         p->nband = d->nband;
+        P.nband_dbg = d->nband;
     }
 
     RowInfo *drows = nullptr;

@@ -27,6 +27,7 @@
 // Backward kernel = D^{-1} scaling + L^T substitution + u += w, writes w (in place) and u.
 // Every load of point x+1 is issued while point x computes (one-point software prefetch).
 #include <algorithm>
+#include <cstdio>
 
 #include "tilu_batch.cuh"
 #include "tilu_common.cuh"
@@ -60,30 +61,54 @@ __device__ __forceinline__ void st_release_cta(int *p, int v)
 }
 __device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
 
-// Spin until *flag >= need (flag in shared or global memory).  A dependency bug must fail loudly,
-// not hang the device: after ~10 s of polling the kernel traps.
-__device__ __forceinline__ int wait_shared(const int *flag, int need)
+// Warp-wide wait until *flag >= need (flag in shared or global memory).  Only lane 0 polls; the
+// warp then reconverges through __syncwarp(), which also orders lane 0's acquire before every
+// lane's subsequent loads.  (Letting all lanes poll is unsafe under independent thread scheduling:
+// lanes can leave the loop at different times while the compiler keeps the warp-uniform row
+// index in a uniform register -- observed as an out-of-range shared access.)  A dependency bug
+// must fail loudly, not hang the device: after ~10 s of polling the kernel traps.
+__device__ __forceinline__ int wait_shared(const int *flag, int need, int lane)
 {
-    long long polls = 0;
-    int v;
-    while ((v = ld_acquire_cta(flag)) < need) {
-        __nanosleep(32);
-        if (++polls > (1ll << 28)) __trap();
+    int v = 0;
+    if (lane == 0) {
+        long long polls = 0;
+        while ((v = ld_acquire_cta(flag)) < need) {
+            __nanosleep(32);
+            if (++polls > (1ll << 28)) __trap();
+        }
     }
-    return v;
+    __syncwarp();
+    return __shfl_sync(0xffffffffu, v, 0);
 }
-__device__ __forceinline__ int wait_global(const int *flag, int need)
+__device__ __forceinline__ int wait_global(const int *flag, int need, int lane)
 {
-    long long polls = 0;
-    int v;
-    while ((v = ld_relaxed(flag)) < need) {
-        __nanosleep(64);
-        if (++polls > (1ll << 27)) __trap();
+    int v = 0;
+    if (lane == 0) {
+        long long polls = 0;
+        while ((v = ld_relaxed(flag)) < need) {
+            __nanosleep(64);
+            if (++polls > (1ll << 27)) __trap();
+        }
     }
-    return v;
+    __syncwarp();
+    return __shfl_sync(0xffffffffu, v, 0);
 }
 
 __device__ __forceinline__ bool in_band_b(int x, int y, int z, int xe) { return z == 1 || y == 1 || x == 1 || x == xe; }
+
+// Debug build (-DTILU_DEBUG_BOUNDS): every packed / table access is range-checked.
+#ifdef TILU_DEBUG_BOUNDS
+#define TILU_CHECK(cond, what, a, b)                                                                  \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("tilu bounds: %s (%lld, %lld) block %d thread %d\n", what, (long long)(a), (long long)(b), \
+                   blockIdx.x, threadIdx.x);                                                          \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define TILU_CHECK(cond, what, a, b) ((void)0)
+#endif
 
 // Sync warp: mirror this layer's per-row progress (shared) to the global array the neighbouring
 // layer polls.  Each round: read all rows, one st.release.gpu (MEMBAR.GPU, cumulative over the
@@ -170,6 +195,7 @@ __device__ __forceinline__ void fwd_load(FwdSlot &S, const double *__restrict__ 
                                          const double *__restrict__ w, const FwdRow &R, int p)
 {
     const uint32_t X = (uint32_t)p * 32u;
+    TILU_CHECK(p >= 1 && p <= R.m, "fwd_load p", p, R.m);
     S.ue = u[R.oc + X + 32];
     S.us = u[R.os + X + 32];
     S.un = u[R.on + X];
@@ -186,8 +212,10 @@ __device__ __forceinline__ void fwd_load(FwdSlot &S, const double *__restrict__ 
 // Lane m < 7 fetches the V1 band-store entry L_m of point p (uniform over the warp's tets).
 __device__ __forceinline__ void fwd_band_load(double &dst, const PlanDev &P, const FwdRow &R, int z, int p, int lane)
 {
-    if (P.variant == 1 && lane < 7 && in_band_b(p, R.y, z, R.m))
+    if (P.variant == 1 && lane < 7 && in_band_b(p, R.y, z, R.m)) {
+        TILU_CHECK(R.boff + ((z == 1 || R.y == 1) ? p - 1 : (p == 1 ? 0 : 1)) < P.nband_dbg, "fwd band", R.boff, p);
         dst = P.store[9 * (int64_t)(R.boff + ((z == 1 || R.y == 1) ? p - 1 : (p == 1 ? 0 : 1))) + lane];
+    }
 }
 
 template <int K, bool EXACT, bool CONST_ROW>
@@ -208,6 +236,7 @@ __global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
     __syncthreads();
     if (A.max_ticket >= 0 && s_ticket > A.max_ticket) return;
     const int nl = P.n - 3, n = P.n;
+    TILU_CHECK(s_ticket < A.G * nl, "fwd ticket", s_ticket, A.G);
     const int zi = s_ticket / A.G, g = s_ticket - (s_ticket / A.G) * A.G;
     const int z = zi + 1, Rn = n - 2 - z;
     int *gp = A.gprog + ((size_t)g * nl + zi) * GSTRIDE;
@@ -227,6 +256,7 @@ __global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
             if (lane == 0) y = atomicAdd(&s_next, 1) + 1;
             y = __shfl_sync(0xffffffffu, y, 0);
             if (y > Rn) break;
+            TILU_CHECK(y >= 1 && y <= Rn && z >= 1 && z <= nl, "fwd row", y, z);
             FwdRow R;
             R.y = y;
             R.m = n - 1 - z - y;
@@ -245,10 +275,10 @@ __global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
             // below: row y (length m+1) up to p+1 and row y+1 (length m) up to p
             int cs = 0, cby = 0, cbn = 0;
             auto ensure = [&](int p) {
-                if (cs < p + 1) cs = wait_shared(&s_prog[y - 1], p + 1);
+                if (cs < p + 1) cs = wait_shared(&s_prog[y - 1], p + 1, lane);
                 if (gb) {
-                    if (cby < p + 1) cby = wait_global(&gb[y], p + 1);
-                    if (cbn < p) cbn = wait_global(&gb[y + 1], p);
+                    if (cby < p + 1) cby = wait_global(&gb[y], p + 1, lane);
+                    if (cbn < p) cbn = wait_global(&gb[y + 1], p, lane);
                 }
             };
             ensure(1);
@@ -363,6 +393,7 @@ __device__ __forceinline__ void bwd_load(BwdSlot &S, const double *__restrict__ 
                                          const BwdRow &R, int x)
 {
     const uint32_t X = (uint32_t)x * 32u;
+    TILU_CHECK(x >= 1 && x <= R.m, "bwd_load x", x, R.m);
     S.wn = w[R.on + X - 32];         // same layer (row y+1): written by a warp of this CTA
     S.wts = ldcg(w + R.ots + X);     // layer above: written by another CTA
     S.wtc = ldcg(w + R.otc + X - 32);
@@ -381,12 +412,14 @@ __device__ __forceinline__ int bwd_band_load(double &dst, const BwdRow &R, const
         const int qx = x - kDX[lane], qy = R.y - kDY[lane], qz = z - kDZ[lane];
         if (!interior(qx, qy, qz, n)) return 0;
         if (P.variant == 1 && (R.qrow_band || qx == 1 || qx == R.qxe)) {
+            TILU_CHECK(R.qboff + (R.qrow_band ? qx - 1 : (qx == 1 ? 0 : 1)) < P.nband_dbg, "bwd band q", R.qboff, qx);
             dst = P.store[9 * (int64_t)(R.qboff + (R.qrow_band ? qx - 1 : (qx == 1 ? 0 : 1))) + lane];
             return 1;
         }
         return 2;
     }
     if (P.variant == 1 && in_band_b(x, R.y, z, R.m)) {
+        TILU_CHECK(R.qboff + ((z == 1 || R.y == 1) ? x - 1 : (x == 1 ? 0 : 1)) < P.nband_dbg, "bwd band p", R.qboff, x);
         dst = P.store[9 * (int64_t)(R.qboff + ((z == 1 || R.y == 1) ? x - 1 : (x == 1 ? 0 : 1))) + 8];
         return 1;
     }
@@ -410,6 +443,7 @@ __global__ void __launch_bounds__(NT, 2) k_batch_bwd(PlanDev P, BatchArgs A)
     __syncthreads();
     if (A.max_ticket >= 0 && s_ticket > A.max_ticket) return;
     const int nl = P.n - 3, n = P.n;
+    TILU_CHECK(s_ticket < A.G * nl, "bwd ticket", s_ticket, A.G);
     const int li = s_ticket / A.G, g = s_ticket - li * A.G;
     const int zi = nl - 1 - li;
     const int z = zi + 1, Rn = n - 2 - z;
@@ -432,6 +466,7 @@ __global__ void __launch_bounds__(NT, 2) k_batch_bwd(PlanDev P, BatchArgs A)
         t = __shfl_sync(0xffffffffu, t, 0);
         const int y = Rn - t;
         if (y < 1) break;
+        TILU_CHECK(y <= Rn && z >= 1 && z <= nl, "bwd row", y, z);
         BwdRow R;
         R.y = y;
         R.m = n - 1 - z - y;
@@ -455,10 +490,10 @@ __global__ void __launch_bounds__(NT, 2) k_batch_bwd(PlanDev P, BatchArgs A)
         int cn = 0, cts = 0, ctc = 0;
         auto ensure = [&](int k) {
             const int k1 = min(k, m - 1);
-            if (cn < k1) cn = wait_shared(&s_prog[y + 1], k1);
+            if (cn < k1) cn = wait_shared(&s_prog[y + 1], k1, lane);
             if (ga) {
-                if (y >= 2 && cts < k) cts = wait_global(&ga[y - 1], k);
-                if (y <= Rn - 1 && ctc < k1) ctc = wait_global(&ga[y], k1);
+                if (y >= 2 && cts < k) cts = wait_global(&ga[y - 1], k, lane);
+                if (y <= Rn - 1 && ctc < k1) ctc = wait_global(&ga[y], k1, lane);
             }
         };
         ensure(1);

@@ -32,6 +32,7 @@ struct PlanDev {
     const double *seedA;             // [nrows][15][akx1] operator-surrogate tables or nullptr
     int akx1;
     const double *factors;           // [grid][9] stored ILU rows or nullptr
+    int64_t nband_dbg;               // band entries (debug bounds checks)
 };
 
 }  // namespace tilu
