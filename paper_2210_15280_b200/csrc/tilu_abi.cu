@@ -466,7 +466,9 @@ static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int nt
     if (sweeps == 0) return TILU_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const PlanDev &P = p->dev;
-    if (!stored && batch_ok(p) && ntets >= 2) {
+    // Batched dataflow kernels for several tets, and for one large tet (1 tet in a 32-lane group still
+    // beats the one-CTA-per-tet reference-layout kernels by ~10x from level 6 up: tools/single_tet.py).
+    if (!stored && batch_ok(p) && (ntets >= 2 || P.level >= 6)) {
         // reference layout in, packed sweeps, reference layout out
         Scratch sc(s);
         const size_t pk = packed_doubles(p, ntets);
