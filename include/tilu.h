@@ -100,13 +100,17 @@ int tilu_stencil_apply(const tilu_plan_t *plan, const double *u, double *out, in
 int tilu_sweep(const tilu_plan_t *plan, double *u, const double *f, int ntets, int sweeps,
                double *rnorm2, void *stream);
 
-/* Packed (interleaved) layout for batches of macro-tets sharing one plan: groups of 32 tets,
- * group g = fp64 [grid][32] (tet-minor), i.e. one lattice point of 32 tets is 256 contiguous bytes.
- * tilu_packed_size() = doubles needed for ntets; tilu_pack/unpack convert from/to the reference
- * layout [ntets][grid] (padding tets are zero).  tilu_sweep_packed() runs `sweeps` fused sweeps on
- * packed u, f with caller-owned packed scratch w (must be zero on the lattice boundary, e.g.
- * zero-initialised once).  tilu_sweep() uses this path internally for ntets >= 2. */
+/* Packed (interleaved) layout for batches of macro-tets sharing one plan: groups of GW = 32 * T
+ * tets (T = 2 for ntets > 32, else 1), group g = fp64 [grid][GW] (tet-minor), i.e. one lattice
+ * point of a group is 256 / 512 contiguous bytes.  tilu_packed_size() = doubles of a packed vector
+ * for ntets; tilu_pack/unpack convert from/to the reference layout [ntets][grid] (padding tets are
+ * zero).  tilu_sweep_packed() runs `sweeps` fused sweeps on packed u, f with caller-owned scratch
+ * w_p of tilu_packed_scratch_size() doubles, zero-initialised before its first use (it keeps its
+ * own state across calls: a header plus the two work vectors; reuse it only with the same plan and
+ * ntets, or zero it again).  tilu_sweep() uses this path internally for ntets >= 2 and for single
+ * tets from level 6 up. */
 int64_t tilu_packed_size(const tilu_plan_t *plan, int ntets);
+int64_t tilu_packed_scratch_size(const tilu_plan_t *plan, int ntets);
 int tilu_pack(const tilu_plan_t *plan, const double *src, double *dst, int ntets, void *stream);
 int tilu_unpack(const tilu_plan_t *plan, const double *src, double *dst, int ntets, void *stream);
 int tilu_sweep_packed(const tilu_plan_t *plan, double *u_p, const double *f_p, double *w_p, int ntets, int sweeps,

@@ -45,7 +45,8 @@ EXPORTS = (
     "tilu_surrogate_backward", "tilu_residual", "tilu_stencil_apply", "tilu_sweep",
     "tilu_stored_solve_into", "tilu_stored_sweep", "tilu_factorize_stream", "tilu_last_error",
     "tilu_version", "tilu_last_launch_count", "tilu_plan_grid_size", "tilu_plan_interior_size",
-    "tilu_profile_enable", "tilu_profile_reset", "tilu_profile_read", "tilu_packed_size", "tilu_pack",
+    "tilu_profile_enable", "tilu_profile_reset", "tilu_profile_read", "tilu_packed_size",
+    "tilu_packed_scratch_size", "tilu_pack",
     "tilu_unpack", "tilu_sweep_packed",
 )
 
@@ -82,8 +83,9 @@ def lib():
     L.tilu_plan_grid_size.restype = _L
     L.tilu_plan_interior_size.argtypes = [_P]
     L.tilu_plan_interior_size.restype = _L
-    L.tilu_packed_size.argtypes = [_P, _I]
-    L.tilu_packed_size.restype = _L
+    for name in ("tilu_packed_size", "tilu_packed_scratch_size"):
+        getattr(L, name).argtypes = [_P, _I]
+        getattr(L, name).restype = _L
     for name in ("tilu_pack", "tilu_unpack"):
         getattr(L, name).argtypes = [_P, _P, _P, _I, _P]
         getattr(L, name).restype = _I

@@ -28,10 +28,13 @@ bool launch_residual_sop(const PlanDev &P, const double *u, const double *f, dou
 void launch_reduce_rows(const double *part, int nrows, double *out, int ntets, cudaStream_t s);
 bool launch_simple_solve(const PlanDev &P, bool exact, bool stored, double *w, double *state, double *u, int ntets,
                          int which, cudaStream_t s);
-void launch_pack(const double *src, double *dst, int64_t grid, int ntets, cudaStream_t s);
-void launch_unpack(const double *src, double *dst, int64_t grid, int ntets, cudaStream_t s);
-void launch_batch_norms(const double *part, int nl, int ntets, double *out, cudaStream_t s);
+void launch_pack(const double *src, double *dst, int64_t grid, int ntets, int tpl, cudaStream_t s);
+void launch_unpack(const double *src, double *dst, int64_t grid, int ntets, int tpl, cudaStream_t s);
+void launch_batch_norms(const double *part, int nl, int ntets, int tpl, double *out, cudaStream_t s);
 bool launch_batch_pass(const PlanDev &P, const BatchArgs &A, bool exact, bool fwd, cudaStream_t s);
+bool launch_coef_tables(const PlanDev &P, double *cf, double *cb, cudaStream_t s);
+void launch_arm(const PlanDev &P, double *wa, const unsigned long long *hdr, unsigned long long key, int G, int tpl,
+                cudaStream_t s);
 // plane-layout fast path (tilu_plane.cu)
 void prof_begin(cudaStream_t s);
 void prof_end(const char *name, cudaStream_t s);
@@ -137,23 +140,92 @@ bool valid_plan(const tilu_plan_t *p) { return p != nullptr && p->dev.n > 0; }
 
 bool batch_ok(const tilu_plan_t *p)
 {
-    // packed element offsets are 32-bit: grid * 32 < 2^32 (level <= 9)
+    // packed element offsets are 32-bit: grid * 64 < 2^32 (level <= 9)
     return !(p->flags & TILU_SCHED_SIMPLE) && p->dev.level <= 9 && p->dev.n >= 4 && p->bsched != nullptr;
 }
 
-size_t packed_doubles(const tilu_plan_t *p, int ntets) { return (size_t)((ntets + 31) / 32) * p->dev.grid * 32; }
+// Tets per lane of the packed layout (groups of 32 * tpl tets).  Two tets per lane halve the
+// per-point bookkeeping (dependency checks, tables, band lookups) per DoF once there are enough
+// tets to keep the groups' layer pipelines filled.  TILU_TPL=1|2 overrides (measurement only).
+int batch_tpl(int ntets)
+{
+    static const char *e = std::getenv("TILU_TPL");
+    if (e && (e[0] == '1' || e[0] == '2')) return e[0] - '0';
+    return ntets > 32 ? 2 : 1;
+}
 
-// `sweeps` fused sweeps on packed vectors (u, f, w all [G][grid][32]; w zero on the boundary).
-int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp, int ntets, int sweeps,
+// Per-point coefficient tables (2 x [grid][8] doubles, shared by all tets of a batch) replace the
+// per-warp NDDF march for large batches: 46 MB at level 7 (L2-resident), 360 MB at level 8.  Built
+// on first use; TILU_TAB=0|1 overrides the choice (measurement only).
+static std::mutex g_coef_mu;
+static bool want_tables(const tilu_plan_t *p, int ntets)
+{
+    static const char *e = std::getenv("TILU_TAB");
+    if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1' && p->dev.level <= 8;
+    return batch_tpl(ntets) == 2 && p->dev.level <= 8;
+}
+static int ensure_tables(const tilu_plan_t *cp, cudaStream_t s)
+{
+    std::lock_guard<std::mutex> lk(g_coef_mu);
+    tilu_plan_t *p = const_cast<tilu_plan_t *>(cp);
+    if (p->coef) return TILU_OK;
+    const size_t nd = (size_t)p->dev.grid * 8;
+    void *d = nullptr;
+    if (cudaMalloc(&d, 2 * nd * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(TILU_ENOMEM, "coefficient tables: out of device memory");
+    }
+    double *cf = static_cast<double *>(d), *cb = cf + nd;
+    cudaMemsetAsync(d, 0, 2 * nd * sizeof(double), s);
+    if (!launch_coef_tables(p->dev, cf, cb, s)) {
+        cudaFree(d);
+        return fail(TILU_EUNSUPPORTED, "kx+1 = %d not compiled", p->dev.kx1);
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+        cudaFree(d);
+        return check_cuda("coefficient tables");
+    }
+    p->coef = d;
+    p->dev.coefF = cf;
+    p->dev.coefB = cb;
+    return TILU_OK;
+}
+
+size_t packed_doubles(const tilu_plan_t *p, int ntets)
+{
+    const int gw = 32 * batch_tpl(ntets);
+    return (size_t)((ntets + gw - 1) / gw) * p->dev.grid * gw;
+}
+
+// Scratch of the packed path: [header: 8 doubles][w_f: packed][w_b: packed].  The header holds a
+// key (layout of this plan and batch) when w_f is armed (sentinel on the interior): the backward
+// pass re-arms w_f as it goes and its last warp writes the key, so only the first call on a fresh
+// (zeroed) scratch, or one after a failed call, pays the arming pass.
+constexpr size_t kScratchHdr = 8;
+size_t packed_scratch_doubles(const tilu_plan_t *p, int ntets) { return kScratchHdr + 2 * packed_doubles(p, ntets); }
+
+static unsigned long long scratch_key(const tilu_plan_t *p, int ntets)
+{
+    return 0x74696C7500000000ull ^ ((unsigned long long)(uint32_t)ntets << 12) ^
+           ((unsigned long long)batch_tpl(ntets) << 8) ^ (unsigned long long)p->dev.level;
+}
+
+// `sweeps` fused sweeps on packed vectors (u, f [G][grid][32 * tpl]; ws = packed scratch).
+int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *ws, int ntets, int sweeps,
                   double *rnorm2, cudaStream_t s)
 {
     const PlanDev &P = p->dev;
-    const int G = (ntets + 31) / 32, nl = P.n - 3;
+    const int tpl = batch_tpl(ntets), gw = 32 * tpl;
+    const int G = (ntets + gw - 1) / gw;
+    if (want_tables(p, ntets) && !p->coef) {
+        const int rc = ensure_tables(p, s);
+        if (rc) return rc;
+    }
+    PlanDev PK = P;  // kernels see the tables only when this batch wants them
+    if (!want_tables(p, ntets)) PK.coefF = PK.coefB = nullptr;
     Scratch sc(s);
-    // sync block per pass: [ticket, pad, progress[G][nl][GSTRIDE]] ints, zeroed before each pass
-    const size_t npass = 4 + (size_t)G * nl * GSTRIDE;
-    int *sync = reinterpret_cast<int *>(sc.get(npass));  // 2 passes' worth of ints (npass doubles)
-    double *part = rnorm2 ? sc.get((size_t)G * nl * 32) : nullptr;
+    int *sync = reinterpret_cast<int *>(sc.get(2));  // fwd ticket, bwd ticket, bwd done
+    double *part = rnorm2 ? sc.get((size_t)G * P.nrows * gw) : nullptr;
     if (!sync || (rnorm2 && !part)) return fail(TILU_ENOMEM, "scratch allocation failed");
     const bool exact = !(p->flags & TILU_FAST);
     BatchArgs A{};
@@ -161,28 +233,35 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *wp
     A.max_ticket = mt ? std::atoi(mt) : -1;
     A.u = up;
     A.f = fp;
-    A.w = wp;
+    A.hdr = reinterpret_cast<unsigned long long *>(ws);
+    A.wa = ws + kScratchHdr;
+    A.wb = A.wa + packed_doubles(p, ntets);
+    A.key = scratch_key(p, ntets);
     A.G = G;
     A.ntets = ntets;
+    A.tpl = tpl;
     std::memcpy(A.arow, p->harow, sizeof(A.arow));
+    prof_begin(s);
+    launch_arm(P, A.wa, A.hdr, A.key, G, tpl, s);  // no-op when the scratch is armed
+    prof_end("arm", s);
+    ++g_launches;
     for (int k = 0; k < sweeps; ++k) {
-        cudaMemsetAsync(sync, 0, 2 * npass * sizeof(int), s);
+        cudaMemsetAsync(sync, 0, 4 * sizeof(int), s);
         A.ticket = sync;
-        A.gprog = sync + 4;
         A.part = part;
         prof_begin(s);
-        bool ok = launch_batch_pass(P, A, exact, true, s);
+        bool ok = launch_batch_pass(PK, A, exact, true, s);
         prof_end("batch_fwd", s);
-        A.ticket = sync + npass;
-        A.gprog = sync + npass + 4;
+        A.ticket = sync + 1;
+        A.done = sync + 2;
         A.part = nullptr;
         prof_begin(s);
-        ok = ok && launch_batch_pass(P, A, exact, false, s);
+        ok = ok && launch_batch_pass(PK, A, exact, false, s);
         prof_end("batch_bwd", s);
         if (!ok) return fail(TILU_EUNSUPPORTED, "kx+1 = %d not compiled", P.kx1);
         g_launches += 2;
         if (rnorm2) {
-            launch_batch_norms(part, nl, ntets, rnorm2 + (int64_t)k * ntets, s);
+            launch_batch_norms(part, P.nrows, ntets, tpl, rnorm2 + (int64_t)k * ntets, s);
             ++g_launches;
         }
     }
@@ -239,6 +318,7 @@ void tilu_plan_destroy(tilu_plan_t *p)
 {
     if (!p) return;
     for (int i = 0; i < p->nallocs; ++i) cudaFree(p->allocs[i]);
+    if (p->coef) cudaFree(p->coef);
     delete p;
 }
 
@@ -374,6 +454,20 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
         P.seedA = dseedA;
     }
     p->bsched = (n - 3 <= MAXR) ? reinterpret_cast<const void *>(1) : nullptr;  // batched path supports this level
+    {
+        std::vector<std::pair<std::pair<int, int>, int>> keyed;  // ((2y + 3z, z), (z << 10) | y)
+        for (int z = 1; z <= n - 3; ++z)
+            for (int y = 1; y <= n - 2 - z; ++y) keyed.push_back({{2 * y + 3 * z, z}, (z << 10) | y});
+        std::sort(keyed.begin(), keyed.end());
+        std::vector<int> order;
+        for (auto &k : keyed) order.push_back(k.second);
+        int *dorder = nullptr;
+        if ((rc = dev_upload(p, &dorder, order.data(), order.size()))) {
+            tilu_plan_destroy(p);
+            return rc;
+        }
+        P.order = dorder;
+    }
     launch_seed(P, dl, dd, dseedF, dseedB, 0);
     if (d->acoefs) launch_seed_op(P, dacoefs, d->aky1, d->akz1, dseedA, 0);
     if (cudaDeviceSynchronize() != cudaSuccess || (rc = check_cuda("seed tables"))) {
@@ -472,19 +566,19 @@ static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int nt
         // reference layout in, packed sweeps, reference layout out
         Scratch sc(s);
         const size_t pk = packed_doubles(p, ntets);
-        double *up = sc.get(pk), *fp = sc.get(pk), *wp = sc.get(pk);
+        double *up = sc.get(pk), *fp = sc.get(pk), *wp = sc.get(packed_scratch_doubles(p, ntets));
         if (!up || !fp || !wp) return fail(TILU_ENOMEM, "scratch allocation failed");
-        cudaMemsetAsync(wp, 0, pk * sizeof(double), s);
+        cudaMemsetAsync(wp, 0, kScratchHdr * sizeof(double), s);  // header 0: arm on first use
         prof_begin(s);
-        launch_pack(u, up, P.grid, ntets, s);
-        launch_pack(f, fp, P.grid, ntets, s);
+        launch_pack(u, up, P.grid, ntets, batch_tpl(ntets), s);
+        launch_pack(f, fp, P.grid, ntets, batch_tpl(ntets), s);
         prof_end("pack", s);
         int rc = packed_sweeps(p, up, fp, wp, ntets, sweeps, rnorm2, s);
         if (rc) return rc;
         prof_begin(s);
-        launch_unpack(up, u, P.grid, ntets, s);
+        launch_unpack(up, u, P.grid, ntets, batch_tpl(ntets), s);
         prof_end("unpack", s);
-        g_launches += 3;
+        g_launches += 3;  // + the sweeps' own launches counted by packed_sweeps
         return check_cuda("batched sweep");
     }
     Scratch sc(s);
@@ -513,12 +607,16 @@ int64_t tilu_packed_size(const tilu_plan_t *p, int ntets)
 {
     return (p && ntets > 0) ? (int64_t)packed_doubles(p, ntets) : -1;
 }
+int64_t tilu_packed_scratch_size(const tilu_plan_t *p, int ntets)
+{
+    return (p && ntets > 0) ? (int64_t)packed_scratch_doubles(p, ntets) : -1;
+}
 
 int tilu_pack(const tilu_plan_t *p, const double *src, double *dst, int ntets, void *stream)
 {
     g_launches = 0;
     if (!valid_plan(p) || !src || !dst || ntets < 1) return fail(TILU_EINVAL, "invalid arguments");
-    launch_pack(src, dst, p->dev.grid, ntets, static_cast<cudaStream_t>(stream));
+    launch_pack(src, dst, p->dev.grid, ntets, batch_tpl(ntets), static_cast<cudaStream_t>(stream));
     g_launches = 1;
     return check_cuda("pack");
 }
@@ -527,7 +625,7 @@ int tilu_unpack(const tilu_plan_t *p, const double *src, double *dst, int ntets,
 {
     g_launches = 0;
     if (!valid_plan(p) || !src || !dst || ntets < 1) return fail(TILU_EINVAL, "invalid arguments");
-    launch_unpack(src, dst, p->dev.grid, ntets, static_cast<cudaStream_t>(stream));
+    launch_unpack(src, dst, p->dev.grid, ntets, batch_tpl(ntets), static_cast<cudaStream_t>(stream));
     g_launches = 1;
     return check_cuda("unpack");
 }

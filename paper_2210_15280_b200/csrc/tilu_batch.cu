@@ -1,30 +1,30 @@
 // Batched fast path: many macro-tets that share one surrogate (identical operator, e.g. the
 // 384 Kuhn tets of config 4) swept together in an interleaved layout.
 //
-// Layout ("packed"): tets are grouped by 32; group g stores fp64 [grid][32], i.e. the 32 tets'
-// values of one lattice point are one 256-byte segment.  A warp processes one lattice row for
-// the 32 tets of its group (lane = tet), so every load and store of u, f, w is a fully
-// coalesced 256 B access, no lane is ever idle, and each lane executes exactly the reference's
-// serial operation sequence for its own tet (bitwise parity in exact mode).
+// Layout ("packed"): tets are grouped by GW = 32 * T (T = tets per lane, 1 or 2); group g stores
+// fp64 [grid][GW], i.e. the GW tets' values of one lattice point are one contiguous 256 / 512 B
+// segment.  A warp processes one lattice row for the tets of its group (lane = T tets), so every
+// load and store of u, f, w is a fully coalesced access, no lane is ever idle, and each lane
+// executes exactly the reference's serial operation sequence for its own tets (bitwise parity in
+// exact mode).
 //
-// Execution: dataflow, no barriers on the compute path.  One CTA per (group, z-layer); CTAs take
-// tickets in dependency order (ascending z forward, descending backward), so a CTA only ever
-// waits for CTAs that already run: deadlock-free for any residency.  Inside a CTA, BW compute
-// warps claim the layer's rows one at a time from a shared counter (in y order forward, reverse
-// order backward) and each publishes its row's progress (points done) in shared memory with
-// st.release.cta after every point.  Before touching point x (and the point it prefetches) a warp
-// checks exactly the rows it reads: the previous row of its own layer (shared memory,
-// ld.acquire.cta = plain LDS) and the two rows of the neighbouring layer (global progress array,
-// relaxed gpu-scope loads, cached in registers and re-polled only when insufficient).  One sync
-// warp per CTA mirrors the shared progress array to global memory behind one st.release.gpu
-// (MEMBAR.GPU, cumulative over what it observed) per round, off the compute path.
-// Polling uses relaxed loads: ld.acquire.gpu / __threadfence emit CCTL.IVALL on sm_100a (whole-L1
-// invalidation) and would wipe the u reuse in L1; a consumer never touches a w line before its
-// producer wrote it, and cross-layer data is read with ld.global.cg after the progress value has
-// returned, so no stale copy can be observed.
+// Execution: fence-free dataflow.  The data is the flag: the two work vectors (w_f written by the
+// forward pass, w_b by the backward pass) hold a signalling-NaN sentinel at every interior point
+// until the point's final value is stored.  Arithmetic never produces a signalling NaN (results
+// are quieted), so a consumer that reads a non-sentinel value has the final value; aligned 8-byte
+// accesses are single-copy atomic, so nothing can be torn, and no ordering between different
+// points is needed -- no progress flags, no fences (a per-point release fence would wait for the
+// software-prefetch loads in flight and serialise every point on memory latency).  A consumer
+// re-reads (L2, ld.global.cg) a neighbour value that is still the sentinel.
 //
-// Forward kernel  = residual f - A u (15-point stencil) + forward L substitution, writes w.
-// Backward kernel = D^{-1} scaling + L^T substitution + u += w, writes w (in place) and u.
+// Scheduling: persistent warps take single rows (for one group) from one global ticket counter in
+// wavefront order t = 2y + 3z (ascending forward, descending backward).  Every dependency of a row
+// has a strictly smaller t, so a warp only ever waits for rows already taken by running warps:
+// deadlock-free for any residency, and perfectly load-balanced.
+//
+// Forward kernel  = residual f - A u (15-point stencil) + forward L substitution: writes w_f, and
+//                   re-arms w_b (sentinel) for the backward pass.
+// Backward kernel = D^{-1} scaling + L^T substitution + u += w: writes w_b and u, re-arms w_f.
 // Every load of point x+1 is issued while point x computes (one-point software prefetch).
 #include <algorithm>
 #include <cstdio>
@@ -35,31 +35,46 @@
 
 namespace tilu {
 
-__device__ __forceinline__ int ld_relaxed(const int *p)
+constexpr int kWarps = 4;  // warps per CTA (independent; the CTA is only an occupancy unit)
+constexpr long long kSent = 0x7FF4DEADBEEF0001ll;  // signalling NaN: "not yet computed"
+
+// T tets per lane (T = 1: groups of 32 tets; T = 2: groups of 64, one 16-byte access per lane).
+template <int T>
+struct Vt {
+    double a[T];
+};
+template <int T>
+__device__ __forceinline__ Vt<T> ldv(const double *p)
 {
-    int v;
-    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+    Vt<T> r;
+    if constexpr (T == 1) {
+        r.a[0] = *p;
+    } else {
+        const double2 d = *reinterpret_cast<const double2 *>(p);
+        r.a[0] = d.x;
+        r.a[1] = d.y;
+    }
+    return r;
 }
-__device__ __forceinline__ void st_release(int *p, int v)
+template <int T>
+__device__ __forceinline__ Vt<T> ldcgv(const double *p)
 {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    Vt<T> r;
+    if constexpr (T == 1) {
+        r.a[0] = __ldcg(p);
+    } else {
+        const double2 d = __ldcg(reinterpret_cast<const double2 *>(p));
+        r.a[0] = d.x;
+        r.a[1] = d.y;
+    }
+    return r;
 }
-__device__ __forceinline__ void st_relaxed(int *p, int v)
+template <int T>
+__device__ __forceinline__ void stv(double *p, const Vt<T> &v)
 {
-    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    if constexpr (T == 1) *p = v.a[0];
+    else *reinterpret_cast<double2 *>(p) = make_double2(v.a[0], v.a[1]);
 }
-__device__ __forceinline__ int ld_acquire_cta(const int *p)
-{
-    int v;
-    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_cta(int *p, int v)
-{
-    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
 
 // Warp-wide wait until *flag >= need (flag in shared or global memory).  Only lane 0 polls; the
 // warp then reconverges through __syncwarp(), which also orders lane 0's acquire before every
@@ -67,34 +82,40 @@ __device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
 // lanes can leave the loop at different times while the compiler keeps the warp-uniform row
 // index in a uniform register -- observed as an out-of-range shared access.)  A dependency bug
 // must fail loudly, not hang the device: after ~10 s of polling the kernel traps.
-__device__ __forceinline__ int wait_shared(const int *flag, int need, int lane)
+__device__ __forceinline__ bool is_sent(double v) { return __double_as_longlong(v) == kSent; }
+template <int T>
+__device__ __forceinline__ bool any_sent(const Vt<T> &v)
 {
-    int v = 0;
-    if (lane == 0) {
-        long long polls = 0;
-        while ((v = ld_acquire_cta(flag)) < need) {
-            __nanosleep(32);
-            if (++polls > (1ll << 28)) __trap();
-        }
-    }
-    __syncwarp();
-    return __shfl_sync(0xffffffffu, v, 0);
+    bool b = false;
+#pragma unroll
+    for (int t = 0; t < T; ++t) b |= is_sent(v.a[t]);
+    return b;
 }
-__device__ __forceinline__ int wait_global(const int *flag, int need, int lane)
+template <int T>
+__device__ __forceinline__ Vt<T> sent_v()
 {
-    int v = 0;
-    if (lane == 0) {
-        long long polls = 0;
-        while ((v = ld_relaxed(flag)) < need) {
-            __nanosleep(64);
-            if (++polls > (1ll << 27)) __trap();
-        }
+    Vt<T> r;
+#pragma unroll
+    for (int t = 0; t < T; ++t) r.a[t] = __longlong_as_double(kSent);
+    return r;
+}
+
+// Wait until no lane of the warp holds the sentinel in v (re-reading p from L2).  Warp-uniform
+// loop (__any_sync), so lanes never diverge around it; a dependency bug must fail loudly, not hang
+// the device: after ~2^26 re-reads the kernel traps.
+template <int T>
+__device__ __forceinline__ void ready(Vt<T> &v, const double *p)
+{
+    long long spins = 0;
+    while (__any_sync(0xffffffffu, any_sent(v))) {
+        __nanosleep(32);
+        v = ldcgv<T>(p);
+        if (++spins > (1ll << 26)) __trap();
     }
-    __syncwarp();
-    return __shfl_sync(0xffffffffu, v, 0);
 }
 
 __device__ __forceinline__ bool in_band_b(int x, int y, int z, int xe) { return z == 1 || y == 1 || x == 1 || x == xe; }
+
 
 // Debug build (-DTILU_DEBUG_BOUNDS): every packed / table access is range-checked.
 #ifdef TILU_DEBUG_BOUNDS
@@ -110,30 +131,15 @@ __device__ __forceinline__ bool in_band_b(int x, int y, int z, int xe) { return 
 #define TILU_CHECK(cond, what, a, b) ((void)0)
 #endif
 
-// Sync warp: mirror this layer's per-row progress (shared) to the global array the neighbouring
-// layer polls.  Each round: read all rows, one st.release.gpu (MEMBAR.GPU, cumulative over the
-// observed progress and thus over the w stores it covers), then relaxed stores of the values.
-__device__ __forceinline__ void progress_mirror(const int *s_prog, const int *s_done, int *gp, int R, int lane)
+// 8 coefficients of one point (uniform address across the warp: one broadcast transaction each).
+__device__ __forceinline__ void ld_coef(double (&c)[8], const double *p)
 {
-    constexpr int PER = (MAXR + 31) / 32;
-    for (;;) {
-        const int done = ld_acquire_cta(s_done);
-        int v[PER];
+    const double2 *q = reinterpret_cast<const double2 *>(p);
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int y = lane + 1 + 32 * k;
-            v[k] = y <= R ? ld_acquire_cta(&s_prog[y]) : 0;
-        }
-        __syncwarp();
-        if (lane == 0) st_release(&gp[MAXR + 2], done);  // the MEMBAR.GPU of this round
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int y = lane + 1 + 32 * k;
-            if (y <= R) st_relaxed(&gp[y], v[k]);
-        }
-        if (done >= R) return;  // `done` was read before the values: they are final
-        __nanosleep(256);
+    for (int i = 0; i < 4; ++i) {
+        const double2 d = __ldg(q + i);
+        c[2 * i] = d.x;
+        c[2 * i + 1] = d.y;
     }
 }
 
@@ -182,8 +188,9 @@ __device__ __forceinline__ void smem_march(double *tab, int lane)
 // ----------------------------------------------------------------------------------------------
 // forward: residual + L solve
 // ----------------------------------------------------------------------------------------------
+template <int T>
 struct FwdSlot {
-    double ue, us, un, ubn, ubc, uts, utc, f, ws, wbn, wbc;
+    Vt<T> ue, us, un, ubn, ubc, uts, utc, f, ws, wbn, wbc;
 };
 
 struct FwdRow {
@@ -191,22 +198,26 @@ struct FwdRow {
     uint32_t oc, os, on, obn, obc, ots, otc;
 };
 
-__device__ __forceinline__ void fwd_load(FwdSlot &S, const double *__restrict__ u, const double *__restrict__ f,
-                                         const double *__restrict__ w, const FwdRow &R, int p)
+// Offsets (R.o*) are in doubles of the packed group: point index * GW.  w values of neighbouring
+// rows are produced concurrently by other warps: read from L2 (.cg), possibly still the sentinel.
+template <int T>
+__device__ __forceinline__ void fwd_load(FwdSlot<T> &S, const double *__restrict__ u, const double *__restrict__ f,
+                                         const double *w, const FwdRow &R, int p)
 {
-    const uint32_t X = (uint32_t)p * 32u;
+    constexpr uint32_t GW = 32u * T;
+    const uint32_t X = (uint32_t)p * GW;
     TILU_CHECK(p >= 1 && p <= R.m, "fwd_load p", p, R.m);
-    S.ue = u[R.oc + X + 32];
-    S.us = u[R.os + X + 32];
-    S.un = u[R.on + X];
-    S.ubn = u[R.obn + X];
-    S.ubc = u[R.obc + X + 32];
-    S.uts = u[R.ots + X + 32];
-    S.utc = u[R.otc + X];
-    S.f = f[R.oc + X];
-    S.ws = w[R.os + X + 32];          // same layer: written by a warp of this CTA
-    S.wbn = ldcg(w + R.obn + X);      // layer below: written by another CTA
-    S.wbc = ldcg(w + R.obc + X + 32);
+    S.ue = ldv<T>(u + R.oc + X + GW);
+    S.us = ldv<T>(u + R.os + X + GW);
+    S.un = ldv<T>(u + R.on + X);
+    S.ubn = ldv<T>(u + R.obn + X);
+    S.ubc = ldv<T>(u + R.obc + X + GW);
+    S.uts = ldv<T>(u + R.ots + X + GW);
+    S.utc = ldv<T>(u + R.otc + X);
+    S.f = ldv<T>(f + R.oc + X);
+    S.ws = ldcgv<T>(w + R.os + X + GW);
+    S.wbn = ldcgv<T>(w + R.obn + X);
+    S.wbc = ldcgv<T>(w + R.obc + X + GW);
 }
 
 // Lane m < 7 fetches the V1 band-store entry L_m of point p (uniform over the warp's tets).
@@ -218,168 +229,167 @@ __device__ __forceinline__ void fwd_band_load(double &dst, const PlanDev &P, con
     }
 }
 
-template <int K, bool EXACT, bool CONST_ROW>
-__global__ void __launch_bounds__(NT, 2) k_batch_fwd(PlanDev P, BatchArgs A)
+template <int K, bool EXACT, bool CONST_ROW, int T, bool TAB>
+__global__ void __launch_bounds__(kWarps * 32, 4 / T) k_batch_fwd(PlanDev P, BatchArgs A)
 {
-    __shared__ int s_ticket, s_next, s_done;
-    __shared__ int s_prog[MAXR + 2];
-    __shared__ double s_red[BW][32];
-    __shared__ double s_tab[BW][7 * K];
-    __shared__ double s_L[BW][8];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
-        s_ticket = atomicAdd(A.ticket, 1);
-        s_next = 0;
-        s_done = 0;
-    }
-    for (int i = threadIdx.x; i < MAXR + 2; i += NT) s_prog[i] = i == 0 ? (1 << 30) : 0;  // row 0: boundary
-    __syncthreads();
-    if (A.max_ticket >= 0 && s_ticket > A.max_ticket) return;
-    const int nl = P.n - 3, n = P.n;
-    TILU_CHECK(s_ticket < A.G * nl, "fwd ticket", s_ticket, A.G);
-    const int zi = s_ticket / A.G, g = s_ticket - (s_ticket / A.G) * A.G;
-    const int z = zi + 1, Rn = n - 2 - z;
-    int *gp = A.gprog + ((size_t)g * nl + zi) * GSTRIDE;
-    const int *gb = z > 1 ? gp - GSTRIDE : nullptr;  // layer below
-    double ss = 0.0;
-    if (warp == BW) {
-        progress_mirror(s_prog, &s_done, gp, Rn, lane);
-    } else {
-        const size_t gbase = (size_t)g * P.grid * 32 + lane;
+    constexpr uint32_t GW = 32u * T;
+    __shared__ double s_tab[kWarps][7 * K];
+    __shared__ double s_L[kWarps][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n = P.n;
+    const int total = P.nrows * A.G;
+    double *tab = s_tab[warp];
+    double *sL = s_L[warp];
+    for (;;) {
+        int tk = 0;
+        if (lane == 0) tk = atomicAdd(A.ticket, 1);
+        tk = __shfl_sync(0xffffffffu, tk, 0);
+        if (tk >= total || (A.max_ticket >= 0 && tk > A.max_ticket)) break;
+        if (tk == 0 && lane == 0) A.hdr[0] = 0;  // scratch busy until the backward pass completes
+        const int ri = tk / A.G, g = tk - ri * A.G;
+        const int zy = P.order[ri], z = zy >> 10, y = zy & 1023;
+        TILU_CHECK(y >= 1 && z >= 1 && y + z <= n - 2, "fwd row", y, z);
+        const size_t gbase = (size_t)g * P.grid * GW + (size_t)lane * T;
         const double *__restrict__ u = A.u + gbase;
         const double *__restrict__ f = A.f + gbase;
-        double *__restrict__ w = A.w + gbase;
-        double *tab = s_tab[warp];
-        double *sL = s_L[warp];
-        for (;;) {
-            int y = 0;
-            if (lane == 0) y = atomicAdd(&s_next, 1) + 1;
-            y = __shfl_sync(0xffffffffu, y, 0);
-            if (y > Rn) break;
-            TILU_CHECK(y >= 1 && y <= Rn && z >= 1 && z <= nl, "fwd row", y, z);
-            FwdRow R;
-            R.y = y;
-            R.m = n - 1 - z - y;
-            R.rid = row_id(n, z, y);
-            R.oc = (uint32_t)row_offset(n, z, y) * 32u;
-            R.os = (uint32_t)row_offset(n, z, y - 1) * 32u;
-            R.on = (uint32_t)row_offset(n, z, y + 1) * 32u;
-            R.obn = (uint32_t)row_offset(n, z - 1, y + 1) * 32u;
-            R.obc = (uint32_t)row_offset(n, z - 1, y) * 32u;
-            R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
-            R.otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
-            R.boff = P.variant == 1 ? P.bandoff[R.rid] : 0;
-            const int m = R.m;
-            smem_load_table<7, K>(tab, P.seedF + (int64_t)R.rid * 7 * K, lane);
-            // dependencies of point p: row y-1 of this layer (length m+1) up to p+1; the layer
-            // below: row y (length m+1) up to p+1 and row y+1 (length m) up to p
-            int cs = 0, cby = 0, cbn = 0;
-            auto ensure = [&](int p) {
-                if (cs < p + 1) cs = wait_shared(&s_prog[y - 1], p + 1, lane);
-                if (gb) {
-                    if (cby < p + 1) cby = wait_global(&gb[y], p + 1, lane);
-                    if (cbn < p) cbn = wait_global(&gb[y + 1], p, lane);
-                }
-            };
-            ensure(1);
-            // sliding windows (values of point x-1 / x that point x+1 reuses) and point 1
-            double u_wm = u[R.oc], u_c = u[R.oc + 32], us0 = u[R.os + 32], un_m = u[R.on], ubn_m = u[R.obn];
-            double ubc0 = u[R.obc + 32], uts0 = u[R.ots + 32], utc_m = u[R.otc];
-            double ws0 = w[R.os + 32], wbn_m = ldcg(w + R.obn), wbc0 = ldcg(w + R.obc + 32), wprev = 0.0;
-            FwdSlot C, N;
-            fwd_load(C, u, f, w, R, 1);
-            double cband = 0.0, nband = 0.0;
-            fwd_band_load(cband, P, R, z, 1, lane);
-            for (int x = 1; x <= m; ++x) {
-                const int pn = min(x + 1, m);  // prefetch (at the row end: re-read point m, unused)
-                ensure(pn);
-                fwd_load(N, u, f, w, R, pn);
-                fwd_band_load(nband, P, R, z, pn, lane);
-                double ap[15];
-                const double *a = A.arow;
-                if (!CONST_ROW) {
-                    const double *ar = P.arows + 15 * (int64_t)(R.oc / 32u + x);
+        double *wa = A.wa + gbase;
+        double *wb = A.wb + gbase;
+        FwdRow R;
+        R.y = y;
+        R.m = n - 1 - z - y;
+        R.rid = row_id(n, z, y);
+        R.oc = (uint32_t)row_offset(n, z, y) * GW;
+        R.os = (uint32_t)row_offset(n, z, y - 1) * GW;
+        R.on = (uint32_t)row_offset(n, z, y + 1) * GW;
+        R.obn = (uint32_t)row_offset(n, z - 1, y + 1) * GW;
+        R.obc = (uint32_t)row_offset(n, z - 1, y) * GW;
+        R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * GW;
+        R.otc = (uint32_t)row_offset(n, z + 1, y) * GW;
+        R.boff = P.variant == 1 ? P.bandoff[R.rid] : 0;
+        const int m = R.m;
+        const double *cf = P.coefF + 8 * ((int64_t)(R.oc / GW));  // TAB: coefficients of (0, y, z)
+        if constexpr (!TAB) smem_load_table<7, K>(tab, P.seedF + (int64_t)R.rid * 7 * K, lane);
+        // sliding windows (values of point x-1 / x that point x+1 reuses) and point 1
+        Vt<T> u_wm = ldv<T>(u + R.oc), u_c = ldv<T>(u + R.oc + GW), us0 = ldv<T>(u + R.os + GW);
+        Vt<T> un_m = ldv<T>(u + R.on), ubn_m = ldv<T>(u + R.obn), ubc0 = ldv<T>(u + R.obc + GW);
+        Vt<T> uts0 = ldv<T>(u + R.ots + GW), utc_m = ldv<T>(u + R.otc);
+        Vt<T> ws0 = ldcgv<T>(wa + R.os + GW), wbn_m = ldcgv<T>(wa + R.obn), wbc0 = ldcgv<T>(wa + R.obc + GW), wprev;
+        Vt<T> ss;
 #pragma unroll
-                    for (int i = 0; i < 15; ++i) ap[i] = ar[i];
-                    a = ap;
-                }
-                // residual in stencil_apply order (_kernels.py:255-266), then f - A u
-                double acc = EXACT ? dmul(a[7], u_c) : a[7] * u_c;
-                acc = madd<EXACT>(acc, a[0], u_wm);
-                acc = madd<EXACT>(acc, a[1], us0);
-                acc = madd<EXACT>(acc, a[2], C.us);
-                acc = madd<EXACT>(acc, a[3], ubn_m);
-                acc = madd<EXACT>(acc, a[4], C.ubn);
-                acc = madd<EXACT>(acc, a[5], ubc0);
-                acc = madd<EXACT>(acc, a[6], C.ubc);
-                acc = madd<EXACT>(acc, a[8], C.ue);
-                acc = madd<EXACT>(acc, a[9], C.un);
-                acc = madd<EXACT>(acc, a[10], un_m);
-                acc = madd<EXACT>(acc, a[11], C.uts);
-                acc = madd<EXACT>(acc, a[12], uts0);
-                acc = madd<EXACT>(acc, a[13], C.utc);
-                acc = madd<EXACT>(acc, a[14], utc_m);
-                const double r = dsub(C.f, acc);
-                ss = fma(r, r, ss);
-                // L entries: lane m publishes L_m (band store or the shared NDDF table)
+        for (int t = 0; t < T; ++t) wprev.a[t] = ss.a[t] = 0.0;
+        ready<T>(ws0, wa + R.os + GW);
+        ready<T>(wbc0, wa + R.obc + GW);
+        FwdSlot<T> C, N;
+        fwd_load<T>(C, u, f, wa, R, 1);
+        double cband = 0.0, nband = 0.0;
+        double Lc[8], Ln[8];
+        if constexpr (TAB) ld_coef(Lc, cf + 8);
+        else fwd_band_load(cband, P, R, z, 1, lane);
+        for (int x = 1; x <= m; ++x) {
+            const int pn = min(x + 1, m);  // prefetch (at the row end: re-read point m, unused)
+            fwd_load<T>(N, u, f, wa, R, pn);
+            if constexpr (TAB) ld_coef(Ln, cf + 8 * pn);
+            else fwd_band_load(nband, P, R, z, pn, lane);
+            // stencil row: constant -> kernel-parameter constant bank operands (indices are
+            // compile-time after unrolling; never take the parameter's address: that copies it
+            // to local memory), else the per-point rows of P.arows
+            double a[15];
+#pragma unroll
+            for (int i = 0; i < 15; ++i) a[i] = CONST_ROW ? A.arow[i] : P.arows[15 * (int64_t)(R.oc / GW + x) + i];
+            // L entries: from the coefficient table, or lane m publishes L_m (band store or the
+            // shared NDDF table)
+            double L[7];
+            if constexpr (TAB) {
+#pragma unroll
+                for (int i = 0; i < 7; ++i) L[i] = Lc[i];
+            } else {
                 if (lane < 7) sL[lane] = (P.variant == 1 && in_band_b(x, y, z, m)) ? cband : tab[lane * K];
                 __syncwarp();
-                double v;
-                if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
-                    v = msub<true>(r, sL[0], wprev);
-                    v = msub<true>(v, sL[1], ws0);
-                    v = msub<true>(v, sL[2], C.ws);
-                    v = msub<true>(v, sL[3], wbn_m);
-                    v = msub<true>(v, sL[4], C.wbn);
-                    v = msub<true>(v, sL[5], wbc0);
-                    v = msub<true>(v, sL[6], C.wbc);
-                } else {  // own-row term last: one FMA on the row's dependency chain
-                    v = msub<false>(r, sL[1], ws0);
-                    v = msub<false>(v, sL[2], C.ws);
-                    v = msub<false>(v, sL[3], wbn_m);
-                    v = msub<false>(v, sL[4], C.wbn);
-                    v = msub<false>(v, sL[5], wbc0);
-                    v = msub<false>(v, sL[6], C.wbc);
-                    v = msub<false>(v, sL[0], wprev);
-                }
-                w[R.oc + (uint32_t)x * 32u] = v;
-                smem_march<7, K>(tab, lane);  // ends with __syncwarp: orders this point's stores
-                if (lane == 0) st_release_cta(&s_prog[y], x);
-                u_wm = u_c;
-                u_c = C.ue;
-                us0 = C.us;
-                un_m = C.un;
-                ubn_m = C.ubn;
-                ubc0 = C.ubc;
-                uts0 = C.uts;
-                utc_m = C.utc;
-                ws0 = C.ws;
-                wbn_m = C.wbn;
-                wbc0 = C.wbc;
-                wprev = v;
-                C = N;
-                cband = nband;
-            }
-            if (lane == 0) atomicAdd(&s_done, 1);
-        }
-    }
-    if (A.part) {
-        if (warp < BW) s_red[warp][lane] = ss;
-        __syncthreads();
-        if (warp == 0) {
-            double t = 0.0;
 #pragma unroll
-            for (int k = 0; k < BW; ++k) t += s_red[k][lane];
-            A.part[((int64_t)g * nl + zi) * 32 + lane] = t;
+                for (int i = 0; i < 7; ++i) L[i] = sL[i];
+            }
+            // neighbours' w of point x: final unless still the sentinel (then wait)
+            if (__any_sync(0xffffffffu, any_sent(C.ws) | any_sent(C.wbn) | any_sent(C.wbc))) {
+                const uint32_t X = (uint32_t)x * GW;
+                ready<T>(C.ws, wa + R.os + X + GW);
+                ready<T>(C.wbn, wa + R.obn + X);
+                ready<T>(C.wbc, wa + R.obc + X + GW);
+            }
+            Vt<T> v;
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                // residual in stencil_apply order (_kernels.py:255-266), then f - A u
+                double acc = EXACT ? dmul(a[7], u_c.a[t]) : a[7] * u_c.a[t];
+                acc = madd<EXACT>(acc, a[0], u_wm.a[t]);
+                acc = madd<EXACT>(acc, a[1], us0.a[t]);
+                acc = madd<EXACT>(acc, a[2], C.us.a[t]);
+                acc = madd<EXACT>(acc, a[3], ubn_m.a[t]);
+                acc = madd<EXACT>(acc, a[4], C.ubn.a[t]);
+                acc = madd<EXACT>(acc, a[5], ubc0.a[t]);
+                acc = madd<EXACT>(acc, a[6], C.ubc.a[t]);
+                acc = madd<EXACT>(acc, a[8], C.ue.a[t]);
+                acc = madd<EXACT>(acc, a[9], C.un.a[t]);
+                acc = madd<EXACT>(acc, a[10], un_m.a[t]);
+                acc = madd<EXACT>(acc, a[11], C.uts.a[t]);
+                acc = madd<EXACT>(acc, a[12], uts0.a[t]);
+                acc = madd<EXACT>(acc, a[13], C.utc.a[t]);
+                acc = madd<EXACT>(acc, a[14], utc_m.a[t]);
+                const double r = dsub(C.f.a[t], acc);
+                ss.a[t] = fma(r, r, ss.a[t]);
+                double vv;
+                if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
+                    vv = msub<true>(r, L[0], wprev.a[t]);
+                    vv = msub<true>(vv, L[1], ws0.a[t]);
+                    vv = msub<true>(vv, L[2], C.ws.a[t]);
+                    vv = msub<true>(vv, L[3], wbn_m.a[t]);
+                    vv = msub<true>(vv, L[4], C.wbn.a[t]);
+                    vv = msub<true>(vv, L[5], wbc0.a[t]);
+                    vv = msub<true>(vv, L[6], C.wbc.a[t]);
+                } else {  // own-row term last: one FMA on the row's dependency chain
+                    vv = msub<false>(r, L[1], ws0.a[t]);
+                    vv = msub<false>(vv, L[2], C.ws.a[t]);
+                    vv = msub<false>(vv, L[3], wbn_m.a[t]);
+                    vv = msub<false>(vv, L[4], C.wbn.a[t]);
+                    vv = msub<false>(vv, L[5], wbc0.a[t]);
+                    vv = msub<false>(vv, L[6], C.wbc.a[t]);
+                    vv = msub<false>(vv, L[0], wprev.a[t]);
+                }
+                v.a[t] = vv;
+            }
+            stv<T>(wa + R.oc + (uint32_t)x * GW, v);
+            stv<T>(wb + R.oc + (uint32_t)x * GW, sent_v<T>());  // re-arm w_b for the backward pass
+            if constexpr (!TAB) smem_march<7, K>(tab, lane);
+            u_wm = u_c;
+            u_c = C.ue;
+            us0 = C.us;
+            un_m = C.un;
+            ubn_m = C.ubn;
+            ubc0 = C.ubc;
+            uts0 = C.uts;
+            utc_m = C.utc;
+            ws0 = C.ws;
+            wbn_m = C.wbn;
+            wbc0 = C.wbc;
+            wprev = v;
+            C = N;
+            cband = nband;
+            if constexpr (TAB) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) Lc[i] = Ln[i];
+            }
+        }
+        if (A.part) {
+#pragma unroll
+            for (int t = 0; t < T; ++t) A.part[((int64_t)g * P.nrows + ri) * GW + lane * T + t] = ss.a[t];
         }
     }
 }
 
 // ----------------------------------------------------------------------------------------------
-// backward: D^{-1} + L^T solve + update (rows in descending y, points in descending x)
+// backward: D^{-1} + L^T solve + update (rows in descending t, points in descending x)
 // ----------------------------------------------------------------------------------------------
+template <int T>
 struct BwdSlot {
-    double wn, wts, wtc, wf, u;
+    Vt<T> wn, wts, wtc, wf, u;
 };
 
 struct BwdRow {
@@ -389,16 +399,18 @@ struct BwdRow {
     uint32_t oc, on, ots, otc;
 };
 
-__device__ __forceinline__ void bwd_load(BwdSlot &S, const double *__restrict__ u, const double *__restrict__ w,
-                                         const BwdRow &R, int x)
+template <int T>
+__device__ __forceinline__ void bwd_load(BwdSlot<T> &S, const double *__restrict__ u, const double *wa,
+                                         const double *wb, const BwdRow &R, int x)
 {
-    const uint32_t X = (uint32_t)x * 32u;
+    constexpr uint32_t GW = 32u * T;
+    const uint32_t X = (uint32_t)x * GW;
     TILU_CHECK(x >= 1 && x <= R.m, "bwd_load x", x, R.m);
-    S.wn = w[R.on + X - 32];         // same layer (row y+1): written by a warp of this CTA
-    S.wts = ldcg(w + R.ots + X);     // layer above: written by another CTA
-    S.wtc = ldcg(w + R.otc + X - 32);
-    S.wf = w[R.oc + X];
-    S.u = u[R.oc + X];
+    S.wn = ldcgv<T>(wb + R.on + X - GW);  // neighbours' w_b: produced concurrently
+    S.wts = ldcgv<T>(wb + R.ots + X);
+    S.wtc = ldcgv<T>(wb + R.otc + X - GW);
+    S.wf = ldv<T>(wa + R.oc + X);         // own w_f: final since the forward pass
+    S.u = ldv<T>(u + R.oc + X);
 }
 
 // Lane m < 7 classifies q_m = p - d_m of point (x, y, z) and fetches its band-store entry L_m
@@ -426,116 +438,110 @@ __device__ __forceinline__ int bwd_band_load(double &dst, const BwdRow &R, const
     return 2;
 }
 
-template <int K, bool EXACT>
-__global__ void __launch_bounds__(NT, 2) k_batch_bwd(PlanDev P, BatchArgs A)
+template <int K, bool EXACT, int T, bool TAB>
+__global__ void __launch_bounds__(kWarps * 32, 4 / T) k_batch_bwd(PlanDev P, BatchArgs A)
 {
-    __shared__ int s_ticket, s_next, s_done;
-    __shared__ int s_prog[MAXR + 2];
-    __shared__ double s_tab[BW][8 * K];
-    __shared__ double s_L[BW][8];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
-        s_ticket = atomicAdd(A.ticket, 1);
-        s_next = 0;
-        s_done = 0;
-    }
-    for (int i = threadIdx.x; i < MAXR + 2; i += NT) s_prog[i] = 0;
-    __syncthreads();
-    if (A.max_ticket >= 0 && s_ticket > A.max_ticket) return;
-    const int nl = P.n - 3, n = P.n;
-    TILU_CHECK(s_ticket < A.G * nl, "bwd ticket", s_ticket, A.G);
-    const int li = s_ticket / A.G, g = s_ticket - li * A.G;
-    const int zi = nl - 1 - li;
-    const int z = zi + 1, Rn = n - 2 - z;
-    if (threadIdx.x == 0) s_prog[Rn + 1] = 1 << 30;  // row R+1 of this layer: boundary
-    __syncthreads();
-    int *gp = A.gprog + ((size_t)g * nl + zi) * GSTRIDE;
-    const int *ga = z < nl ? gp + GSTRIDE : nullptr;  // layer above
-    if (warp == BW) {
-        progress_mirror(s_prog, &s_done, gp, Rn, lane);
-        return;
-    }
-    const size_t gbase = (size_t)g * P.grid * 32 + lane;
-    double *__restrict__ u = A.u + gbase;
-    double *__restrict__ w = A.w + gbase;
+    constexpr uint32_t GW = 32u * T;
+    __shared__ double s_tab[kWarps][8 * K];
+    __shared__ double s_L[kWarps][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n = P.n;
+    const int total = P.nrows * A.G;
     double *tab = s_tab[warp];
     double *sL = s_L[warp];
     for (;;) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(&s_next, 1);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        const int y = Rn - t;
-        if (y < 1) break;
-        TILU_CHECK(y <= Rn && z >= 1 && z <= nl, "bwd row", y, z);
+        int tk = 0;
+        if (lane == 0) tk = atomicAdd(A.ticket, 1);
+        tk = __shfl_sync(0xffffffffu, tk, 0);
+        if (tk >= total || (A.max_ticket >= 0 && tk > A.max_ticket)) break;
+        const int rr = tk / A.G, g = tk - rr * A.G, ri = P.nrows - 1 - rr;
+        const int zy = P.order[ri], z = zy >> 10, y = zy & 1023;
+        TILU_CHECK(y >= 1 && z >= 1 && y + z <= n - 2, "bwd row", y, z);
+        const size_t gbase = (size_t)g * P.grid * GW + (size_t)lane * T;
+        double *__restrict__ u = A.u + gbase;
+        double *wa = A.wa + gbase;
+        double *wb = A.wb + gbase;
         BwdRow R;
         R.y = y;
         R.m = n - 1 - z - y;
         R.rid = row_id(n, z, y);
-        R.oc = (uint32_t)row_offset(n, z, y) * 32u;
-        R.on = (uint32_t)row_offset(n, z, y + 1) * 32u;
-        R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * 32u;
-        R.otc = (uint32_t)row_offset(n, z + 1, y) * 32u;
+        R.oc = (uint32_t)row_offset(n, z, y) * GW;
+        R.on = (uint32_t)row_offset(n, z, y + 1) * GW;
+        R.ots = (uint32_t)row_offset(n, z + 1, y - 1) * GW;
+        R.otc = (uint32_t)row_offset(n, z + 1, y) * GW;
         const int m = R.m;
-        if (lane < 8) {  // the row of q_m (lane m) or the own row (lane 7)
+        const double *cb = P.coefB + 8 * ((int64_t)(R.oc / GW));  // TAB: coefficients of (0, y, z)
+        if (!TAB && lane < 8) {  // the row of q_m (lane m) or the own row (lane 7)
             const int qy = lane < 7 ? y - kDY[lane] : y, qz = lane < 7 ? z - kDZ[lane] : z;
             const bool valid = qy >= 1 && qz >= 1 && qy + qz <= n - 2;
             R.qxe = n - 1 - qz - qy;
             R.qrow_band = (qz == 1 || qy == 1);
             R.qboff = (P.variant == 1 && valid) ? P.bandoff[row_id(n, qz, qy)] : 0;
         }
-        smem_load_table<8, K>(tab, P.seedB + (int64_t)R.rid * 8 * K, lane);
-        // dependencies of the k-th point (x = m - k + 1): row y+1 of this layer (length m-1) and
-        // row y of the layer above (length m-1) up to min(k, m-1) points, row y-1 of the layer above
-        // (length m) up to k points
-        int cn = 0, cts = 0, ctc = 0;
-        auto ensure = [&](int k) {
-            const int k1 = min(k, m - 1);
-            if (cn < k1) cn = wait_shared(&s_prog[y + 1], k1, lane);
-            if (ga) {
-                if (y >= 2 && cts < k) cts = wait_global(&ga[y - 1], k, lane);
-                if (y <= Rn - 1 && ctc < k1) ctc = wait_global(&ga[y], k1, lane);
-            }
-        };
-        ensure(1);
-        const uint32_t M = (uint32_t)m * 32u;
-        double wn_hi = w[R.on + M], wts_hi = ldcg(w + R.ots + M + 32), wtc_hi = ldcg(w + R.otc + M), wprev = 0.0;
-        BwdSlot C, N;
-        bwd_load(C, u, w, R, m);
+        if constexpr (!TAB) smem_load_table<8, K>(tab, P.seedB + (int64_t)R.rid * 8 * K, lane);
+        // point m+1 of row y+1 / y-1 (layer z+1) and point m of row y (layer z+1) are on the boundary
+        const uint32_t M = (uint32_t)m * GW;
+        Vt<T> wn_hi = ldcgv<T>(wb + R.on + M), wts_hi = ldcgv<T>(wb + R.ots + M + GW), wtc_hi = ldcgv<T>(wb + R.otc + M);
+        Vt<T> wprev;
+#pragma unroll
+        for (int t = 0; t < T; ++t) wprev.a[t] = 0.0;
+        BwdSlot<T> C, N;
+        bwd_load<T>(C, u, wa, wb, R, m);
         double cband = 0.0, nband = 0.0;
-        int csrc = bwd_band_load(cband, R, P, n, z, m, lane), nsrc = 2;
+        double Lc[8], Ln[8];
+        int csrc = 2, nsrc = 2;
+        if constexpr (TAB) ld_coef(Lc, cb + 8 * m);
+        else csrc = bwd_band_load(cband, R, P, n, z, m, lane);
         for (int k = 1; k <= m; ++k) {
             const int x = m - k + 1;
-            const int kn = min(k + 1, m);  // prefetch the next point (at the row end: re-read x = 1)
-            ensure(kn);
-            const int xn = m - kn + 1;
-            bwd_load(N, u, w, R, xn);
-            nsrc = bwd_band_load(nband, R, P, n, z, xn, lane);
-            if (lane < 8) sL[lane] = csrc == 0 ? 0.0 : (csrc == 1 ? cband : tab[lane * K]);
-            __syncwarp();
-            const double inv_d = sL[7];
-            double v = EXACT ? dmul(inv_d, C.wf) : inv_d * C.wf;
-            if (EXACT) {  // reference order (_kernels.py:404-425)
-                v = msub<true>(v, sL[0], wprev);
-                v = msub<true>(v, sL[1], wn_hi);
-                v = msub<true>(v, sL[2], C.wn);
-                v = msub<true>(v, sL[3], wts_hi);
-                v = msub<true>(v, sL[4], C.wts);
-                v = msub<true>(v, sL[5], wtc_hi);
-                v = msub<true>(v, sL[6], C.wtc);
+            const int xn = max(x - 1, 1);  // prefetch the next point (at the row end: re-read x = 1)
+            bwd_load<T>(N, u, wa, wb, R, xn);
+            if constexpr (TAB) ld_coef(Ln, cb + 8 * xn);
+            else nsrc = bwd_band_load(nband, R, P, n, z, xn, lane);
+            double L[8];
+            if constexpr (TAB) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) L[i] = Lc[i];
             } else {
-                v = msub<false>(v, sL[1], wn_hi);
-                v = msub<false>(v, sL[2], C.wn);
-                v = msub<false>(v, sL[3], wts_hi);
-                v = msub<false>(v, sL[4], C.wts);
-                v = msub<false>(v, sL[5], wtc_hi);
-                v = msub<false>(v, sL[6], C.wtc);
-                v = msub<false>(v, sL[0], wprev);
+                if (lane < 8) sL[lane] = csrc == 0 ? 0.0 : (csrc == 1 ? cband : tab[lane * K]);
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 8; ++i) L[i] = sL[i];
             }
-            const uint32_t X = (uint32_t)x * 32u;
-            w[R.oc + X] = v;
-            u[R.oc + X] = dadd(C.u, v);
-            smem_march<8, K>(tab, lane);  // ends with __syncwarp: orders this point's stores
-            if (lane == 0) st_release_cta(&s_prog[y], k);
+            const uint32_t X = (uint32_t)x * GW;
+            if (__any_sync(0xffffffffu, any_sent(C.wn) | any_sent(C.wts) | any_sent(C.wtc))) {
+                ready<T>(C.wn, wb + R.on + X - GW);
+                ready<T>(C.wts, wb + R.ots + X);
+                ready<T>(C.wtc, wb + R.otc + X - GW);
+            }
+            const double inv_d = L[7];
+            Vt<T> v, un;
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                double vv = EXACT ? dmul(inv_d, C.wf.a[t]) : inv_d * C.wf.a[t];
+                if (EXACT) {  // reference order (_kernels.py:404-425)
+                    vv = msub<true>(vv, L[0], wprev.a[t]);
+                    vv = msub<true>(vv, L[1], wn_hi.a[t]);
+                    vv = msub<true>(vv, L[2], C.wn.a[t]);
+                    vv = msub<true>(vv, L[3], wts_hi.a[t]);
+                    vv = msub<true>(vv, L[4], C.wts.a[t]);
+                    vv = msub<true>(vv, L[5], wtc_hi.a[t]);
+                    vv = msub<true>(vv, L[6], C.wtc.a[t]);
+                } else {
+                    vv = msub<false>(vv, L[1], wn_hi.a[t]);
+                    vv = msub<false>(vv, L[2], C.wn.a[t]);
+                    vv = msub<false>(vv, L[3], wts_hi.a[t]);
+                    vv = msub<false>(vv, L[4], C.wts.a[t]);
+                    vv = msub<false>(vv, L[5], wtc_hi.a[t]);
+                    vv = msub<false>(vv, L[6], C.wtc.a[t]);
+                    vv = msub<false>(vv, L[0], wprev.a[t]);
+                }
+                v.a[t] = vv;
+                un.a[t] = dadd(C.u.a[t], vv);
+            }
+            stv<T>(wb + R.oc + X, v);
+            stv<T>(u + R.oc + X, un);
+            stv<T>(wa + R.oc + X, sent_v<T>());  // re-arm w_f for the next forward pass
+            if constexpr (!TAB) smem_march<8, K>(tab, lane);
             wn_hi = C.wn;
             wts_hi = C.wts;
             wtc_hi = C.wtc;
@@ -543,20 +549,97 @@ __global__ void __launch_bounds__(NT, 2) k_batch_bwd(PlanDev P, BatchArgs A)
             C = N;
             cband = nband;
             csrc = nsrc;
+            if constexpr (TAB) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) Lc[i] = Ln[i];
+            }
         }
-        if (lane == 0) atomicAdd(&s_done, 1);
     }
+    // the last warp to finish marks the scratch ready (w_f re-armed everywhere) for the next call
+    if (lane == 0) {
+        __threadfence();
+        if (atomicAdd(A.done, 1) == A.nwarps - 1) {
+            __threadfence();
+            A.hdr[0] = A.key;
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------------------------
+// Coefficient tables: one warp per row runs exactly the on-the-fly evaluation of the kernels above
+// (shared NDDF march + V1 band store + interior classification) and records, per point, the
+// values the sweep kernels would use -- so the TAB kernels are bit-identical to the NDDF ones.
+// ----------------------------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(32) k_coef_tables(PlanDev P, double *__restrict__ cf, double *__restrict__ cb)
+{
+    __shared__ double tab[8 * K];
+    const int lane = threadIdx.x, rid = blockIdx.x, n = P.n;
+    const int z = P.rows[rid].z, y = P.rows[rid].y, m = n - 1 - z - y;
+    const int64_t base = row_offset(n, z, y);
+    // forward
+    FwdRow F;
+    F.y = y;
+    F.m = m;
+    F.rid = rid;
+    F.boff = P.variant == 1 ? P.bandoff[rid] : 0;
+    smem_load_table<7, K>(tab, P.seedF + (int64_t)rid * 7 * K, lane);
+    for (int x = 1; x <= m; ++x) {
+        double band = 0.0;
+        fwd_band_load(band, P, F, z, x, lane);
+        const double v = lane < 7 ? ((P.variant == 1 && in_band_b(x, y, z, m)) ? band : tab[lane * K]) : 0.0;
+        __syncwarp();
+        if (lane < 8) cf[8 * (base + x) + lane] = v;
+        smem_march<7, K>(tab, lane);
+    }
+    __syncwarp();
+    // backward
+    BwdRow B;
+    B.y = y;
+    B.m = m;
+    B.rid = rid;
+    if (lane < 8) {
+        const int qy = lane < 7 ? y - kDY[lane] : y, qz = lane < 7 ? z - kDZ[lane] : z;
+        const bool valid = qy >= 1 && qz >= 1 && qy + qz <= n - 2;
+        B.qxe = n - 1 - qz - qy;
+        B.qrow_band = (qz == 1 || qy == 1);
+        B.qboff = (P.variant == 1 && valid) ? P.bandoff[row_id(n, qz, qy)] : 0;
+    }
+    smem_load_table<8, K>(tab, P.seedB + (int64_t)rid * 8 * K, lane);
+    for (int k = 1; k <= m; ++k) {
+        const int x = m - k + 1;
+        double band = 0.0;
+        const int src = bwd_band_load(band, B, P, n, z, x, lane);
+        const double v = lane >= 8 ? 0.0 : (src == 0 ? 0.0 : (src == 1 ? band : tab[lane * K]));
+        __syncwarp();
+        if (lane < 8) cb[8 * (base + x) + lane] = v;
+        smem_march<8, K>(tab, lane);
+    }
+}
+
+bool launch_coef_tables(const PlanDev &P, double *cf, double *cb, cudaStream_t s)
+{
+#define TILU_CASE(KK) \
+    case KK: k_coef_tables<KK><<<P.nrows, 32, 0, s>>>(P, cf, cb); return true;
+    switch (P.kx1) {
+        TILU_CASE(1) TILU_CASE(2) TILU_CASE(3) TILU_CASE(4) TILU_CASE(5) TILU_CASE(6) TILU_CASE(7) TILU_CASE(8)
+        TILU_CASE(9)
+    default: return false;
+    }
+#undef TILU_CASE
 }
 
 // ----------------------------------------------------------------------------------------------
 // layout conversion and norms
 // ----------------------------------------------------------------------------------------------
-// dst[g][r][l] = src[g*32+l][r] (zero for padded tets): 32x32 tiles through shared memory.
+// dst[g][r][l] = src[g*GW+l][r] (zero for padded tets), GW = 32 * tpl: 32x32 tiles through shared
+// memory, blockIdx.y = 32-tet block b (group b / tpl, lanes 32 * (b % tpl) ...).
 __global__ void __launch_bounds__(256) k_pack(const double *__restrict__ src, double *__restrict__ dst, int64_t grid,
-                                              int ntets)
+                                              int ntets, int tpl)
 {
     __shared__ double tile[32][33];
     const int g = blockIdx.y;
+    const int gw = 32 * tpl, grp = g / tpl, sub = 32 * (g % tpl);
     const int64_t r0 = (int64_t)blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int k = ty; k < 32; k += 8) {
@@ -567,20 +650,21 @@ __global__ void __launch_bounds__(256) k_pack(const double *__restrict__ src, do
     __syncthreads();
     for (int k = ty; k < 32; k += 8) {
         const int64_t r = r0 + k;
-        if (r < grid) dst[((int64_t)g * grid + r) * 32 + tx] = tile[tx][k];
+        if (r < grid) dst[((int64_t)grp * grid + r) * gw + sub + tx] = tile[tx][k];
     }
 }
 
 __global__ void __launch_bounds__(256) k_unpack(const double *__restrict__ src, double *__restrict__ dst, int64_t grid,
-                                                int ntets)
+                                                int ntets, int tpl)
 {
     __shared__ double tile[32][33];
     const int g = blockIdx.y;
+    const int gw = 32 * tpl, grp = g / tpl, sub = 32 * (g % tpl);
     const int64_t r0 = (int64_t)blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int k = ty; k < 32; k += 8) {
         const int64_t r = r0 + k;
-        tile[k][tx] = (r < grid) ? src[((int64_t)g * grid + r) * 32 + tx] : 0.0;
+        tile[k][tx] = (r < grid) ? src[((int64_t)grp * grid + r) * gw + sub + tx] : 0.0;
     }
     __syncthreads();
     for (int k = ty; k < 32; k += 8) {
@@ -590,57 +674,134 @@ __global__ void __launch_bounds__(256) k_unpack(const double *__restrict__ src, 
     }
 }
 
-// rnorm2[t] = sum over layers of the forward kernel's per-(layer, lane) partials, fixed order.
-__global__ void k_batch_norms(const double *__restrict__ part, int nl, int ntets, double *__restrict__ out)
+// Arming an unarmed scratch (header != key): zero w_f and w_b entirely (lattice boundary = 0 in
+// this layout), then w_f := sentinel on the interior (one block per (row, group)).  Both kernels
+// are no-ops when the previous call left the scratch armed.
+__global__ void __launch_bounds__(256) k_arm_zero(double2 *__restrict__ w, int64_t n2, const unsigned long long *hdr,
+                                                  unsigned long long key)
+{
+    if (*hdr == key) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x)
+        w[i] = make_double2(0.0, 0.0);
+}
+
+__global__ void __launch_bounds__(256) k_arm(PlanDev P, double *__restrict__ wa, const unsigned long long *hdr,
+                                             unsigned long long key, int tpl)
+{
+    if (*hdr == key) return;
+    const int rid = blockIdx.x, g = blockIdx.y, gw = 32 * tpl;
+    const int z = P.rows[rid].z, y = P.rows[rid].y, m = P.n - 1 - z - y;
+    double *p = wa + ((size_t)g * P.grid + row_offset(P.n, z, y) + 1) * gw;
+    for (int i = threadIdx.x; i < m * gw; i += blockDim.x) p[i] = __longlong_as_double(kSent);
+}
+
+// rnorm2[t] = sum over rows (wavefront order) of the forward kernel's per-row partials.
+__global__ void k_batch_norms(const double *__restrict__ part, int nrows, int ntets, int gw, double *__restrict__ out)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntets) return;
-    const int g = t / 32, l = t % 32;
+    const int g = t / gw, l = t % gw;
     double s = 0.0;
-    for (int zi = 0; zi < nl; ++zi) s += part[((int64_t)g * nl + zi) * 32 + l];
+    for (int r = 0; r < nrows; ++r) s += part[((int64_t)g * nrows + r) * gw + l];
     out[t] = s;
 }
 
 // ----------------------------------------------------------------------------------------------
 // host launchers
 // ----------------------------------------------------------------------------------------------
-void launch_pack(const double *src, double *dst, int64_t grid, int ntets, cudaStream_t s)
+// padded 32-tet blocks: all blocks of the last group are written (zeros for tets >= ntets)
+static unsigned tet_blocks(int ntets, int tpl) { return (unsigned)(((ntets + 32 * tpl - 1) / (32 * tpl)) * tpl); }
+
+void launch_pack(const double *src, double *dst, int64_t grid, int ntets, int tpl, cudaStream_t s)
+{
+    dim3 gr((unsigned)((grid + 31) / 32), tet_blocks(ntets, tpl));
+    k_pack<<<gr, 256, 0, s>>>(src, dst, grid, ntets, tpl);
+}
+
+void launch_unpack(const double *src, double *dst, int64_t grid, int ntets, int tpl, cudaStream_t s)
 {
     dim3 gr((unsigned)((grid + 31) / 32), (unsigned)((ntets + 31) / 32));
-    k_pack<<<gr, 256, 0, s>>>(src, dst, grid, ntets);
+    k_unpack<<<gr, 256, 0, s>>>(src, dst, grid, ntets, tpl);
 }
 
-void launch_unpack(const double *src, double *dst, int64_t grid, int ntets, cudaStream_t s)
+void launch_batch_norms(const double *part, int nrows, int ntets, int tpl, double *out, cudaStream_t s)
 {
-    dim3 gr((unsigned)((grid + 31) / 32), (unsigned)((ntets + 31) / 32));
-    k_unpack<<<gr, 256, 0, s>>>(src, dst, grid, ntets);
+    k_batch_norms<<<(ntets + 127) / 128, 128, 0, s>>>(part, nrows, ntets, 32 * tpl, out);
 }
 
-void launch_batch_norms(const double *part, int nl, int ntets, double *out, cudaStream_t s)
+void launch_arm(const PlanDev &P, double *wa, const unsigned long long *hdr, unsigned long long key, int G, int tpl,
+                cudaStream_t s)
 {
-    k_batch_norms<<<(ntets + 127) / 128, 128, 0, s>>>(part, nl, ntets, out);
+    const int64_t n2 = (int64_t)G * P.grid * 32 * tpl;  // doubles of w_f + w_b, / 2
+    k_arm_zero<<<4 * 148, 256, 0, s>>>(reinterpret_cast<double2 *>(wa), n2, hdr, key);
+    k_arm<<<dim3((unsigned)P.nrows, (unsigned)G), 256, 0, s>>>(P, wa, hdr, key, tpl);
 }
 
+// Persistent grid: as many CTAs as fit on the device at once (queried once per kernel).
+template <class Kern>
+static unsigned persistent_grid(Kern k)
+{
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kWarps * 32, 0);
+    return (unsigned)std::max(1, sms * std::max(per, 1));
+}
+
+template <int K, int T, bool TAB>
+static void launch_fwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_t s)
+{
+    auto run = [&](auto kern) {
+        static const unsigned grid = persistent_grid(kern);
+        A.nwarps = (int)grid * kWarps;
+        kern<<<grid, kWarps * 32, 0, s>>>(P, A);
+    };
+    const bool c = P.arow != nullptr;
+    if (exact) {
+        if (c) run(k_batch_fwd<K, true, true, T, TAB>);
+        else run(k_batch_fwd<K, true, false, T, TAB>);
+    } else {
+        if (c) run(k_batch_fwd<K, false, true, T, TAB>);
+        else run(k_batch_fwd<K, false, false, T, TAB>);
+    }
+}
+
+template <int K, int T, bool TAB>
+static void launch_bwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_t s)
+{
+    auto run = [&](auto kern) {
+        static const unsigned grid = persistent_grid(kern);
+        A.nwarps = (int)grid * kWarps;
+        kern<<<grid, kWarps * 32, 0, s>>>(P, A);
+    };
+    if (exact) run(k_batch_bwd<K, true, T, TAB>);
+    else run(k_batch_bwd<K, false, T, TAB>);
+}
+
+// T = 1: groups of 32 tets, T = 2: groups of 64 (two tets per lane); coefficients from the
+// per-point tables when the plan has them (large batches), else the on-the-fly NDDF march.
 template <int K>
 static void launch_fwd_k(const PlanDev &P, const BatchArgs &A, bool exact, cudaStream_t s)
 {
-    const unsigned grid = (unsigned)(A.G * (P.n - 3));
-    const bool c = P.arow != nullptr;
-    if (exact) {
-        if (c) k_batch_fwd<K, true, true><<<grid, NT, 0, s>>>(P, A);
-        else k_batch_fwd<K, true, false><<<grid, NT, 0, s>>>(P, A);
+    if (A.tpl == 2) {
+        if (P.coefF) launch_fwd_kt<K, 2, true>(P, A, exact, s);
+        else launch_fwd_kt<K, 2, false>(P, A, exact, s);
     } else {
-        if (c) k_batch_fwd<K, false, true><<<grid, NT, 0, s>>>(P, A);
-        else k_batch_fwd<K, false, false><<<grid, NT, 0, s>>>(P, A);
+        if (P.coefF) launch_fwd_kt<K, 1, true>(P, A, exact, s);
+        else launch_fwd_kt<K, 1, false>(P, A, exact, s);
     }
 }
 
 template <int K>
 static void launch_bwd_k(const PlanDev &P, const BatchArgs &A, bool exact, cudaStream_t s)
 {
-    const unsigned grid = (unsigned)(A.G * (P.n - 3));
-    if (exact) k_batch_bwd<K, true><<<grid, NT, 0, s>>>(P, A);
-    else k_batch_bwd<K, false><<<grid, NT, 0, s>>>(P, A);
+    if (A.tpl == 2) {
+        if (P.coefB) launch_bwd_kt<K, 2, true>(P, A, exact, s);
+        else launch_bwd_kt<K, 2, false>(P, A, exact, s);
+    } else {
+        if (P.coefB) launch_bwd_kt<K, 1, true>(P, A, exact, s);
+        else launch_bwd_kt<K, 1, false>(P, A, exact, s);
+    }
 }
 
 bool launch_batch_pass(const PlanDev &P, const BatchArgs &A, bool exact, bool fwd, cudaStream_t s)

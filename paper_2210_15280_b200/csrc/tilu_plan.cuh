@@ -33,6 +33,14 @@ struct PlanDev {
     int akx1;
     const double *factors;           // [grid][9] stored ILU rows or nullptr
     int64_t nband_dbg;               // band entries (debug bounds checks)
+    // Per-point coefficient tables of the batched path (shared by every tet of a batch; built once
+    // per plan on first use, bit-identical to the on-the-fly NDDF + band evaluation):
+    const double *coefF;             // [grid][8]: L_0..L_6 at p (forward), 0
+    const double *coefB;             // [grid][8]: L_0..L_6 at q_m = p - d_m (0 outside), 1/D at p
+    // Batched row order: (z << 10) | y for every interior row, sorted by the wavefront step of its
+    // first point t = 2y + 3z (ties by z).  Every forward dependency of a row has a smaller t, so
+    // the order is topological; the backward pass walks it reversed.
+    const int *order;
 };
 
 }  // namespace tilu
@@ -45,6 +53,7 @@ struct tilu_plan {
     int64_t interior;
     int64_t nband;
     int ky1a, kz1a;
+    void *coef;  // coefficient tables (2 x [grid][8] doubles), lazily built; freed with the plan
     // owned device allocations
     void *allocs[16];
     int nallocs;

@@ -121,7 +121,7 @@ class MacroMeshSmoother:
             ug, fg = u.index_select(0, idx).contiguous(), f.index_select(0, idx).contiguous()
             p = sm.plan
             up, fp = p.pack(ug), p.pack(fg)
-            wp = torch.zeros_like(up)
+            wp = p.new_scratch(len(g), device=up.device)
             self._res.append((sm, g, up, fp, wp))
 
     def sweep(self, sweeps: int = 1, residual_norms: bool = True):

@@ -156,6 +156,14 @@ class DevicePlan:
     def packed_numel(self, ntets: int) -> int:
         return int(_lib.lib().tilu_packed_size(self._h, int(ntets)))
 
+    def scratch_numel(self, ntets: int) -> int:
+        return int(_lib.lib().tilu_packed_scratch_size(self._h, int(ntets)))
+
+    def new_scratch(self, ntets: int, device="cuda"):
+        """Zeroed scratch for :meth:`sweep_packed` (keeps its own state across calls; reuse it only
+        with this plan and the same ntets)."""
+        return torch.zeros(self.scratch_numel(ntets), dtype=torch.float64, device=device)
+
     def pack(self, src, ntets: int | None = None, out=None):
         src, T = _as_batch(src, self.grid, "src")
         T = T if ntets is None else ntets
@@ -172,11 +180,11 @@ class DevicePlan:
         return out
 
     def sweep_packed(self, u_p, f_p, w_p, ntets: int, sweeps: int = 1, norms: bool = False):
-        """Fused sweeps on packed u, f (w_p: packed scratch, zero on the lattice boundary)."""
-        for name, t in (("u_p", u_p), ("f_p", f_p), ("w_p", w_p)):
-            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
-                    and t.numel() == self.packed_numel(ntets)):
-                raise ValueError(f"{name}: packed CUDA fp64 buffer of {self.packed_numel(ntets)} doubles required")
+        """Fused sweeps on packed u, f (w_p: scratch from :meth:`new_scratch`)."""
+        for name, t, size in (("u_p", u_p, self.packed_numel(ntets)), ("f_p", f_p, self.packed_numel(ntets)),
+                              ("w_p", w_p, self.scratch_numel(ntets))):
+            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and t.numel() == size):
+                raise ValueError(f"{name}: CUDA fp64 buffer of {size} doubles required")
         rn = torch.empty((sweeps, ntets), dtype=torch.float64, device=u_p.device) if norms else None
         _lib.check(_lib.lib().tilu_sweep_packed(self._h, u_p.data_ptr(), f_p.data_ptr(), w_p.data_ptr(), int(ntets),
                                                 int(sweeps), None if rn is None else rn.data_ptr(), _stream_ptr()))

@@ -243,7 +243,7 @@ def test_packed_resident_api_and_roundtrip():
     p.unpack(p.pack(us), back)
     assert torch.equal(back, us)
     up, fp = p.pack(us), p.pack(torch.zeros_like(us))
-    wp = torch.zeros_like(up)
+    wp = p.new_scratch(T)
     p.sweep_packed(up, fp, wp, T, 2)
     ref = us.clone()
     p.sweep(ref, torch.zeros_like(us), 2)     # reference-layout entry point

@@ -28,7 +28,7 @@ u[:, torch.as_tensor(mask, device="cuda")] = torch.rand((a.tets, int(mask.sum())
                                                         device="cuda") * 2 - 1
 up = p.pack(u)
 fp = p.pack(torch.zeros_like(u))
-wp = torch.zeros_like(up)
+wp = p.new_scratch(a.tets)
 for _ in range(a.sweeps):
     p.sweep_packed(up, fp, wp, a.tets, 1, norms=True)
 torch.cuda.synchronize()

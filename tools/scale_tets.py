@@ -17,7 +17,7 @@ grid = lattice.grid_size(level)
 for T in [int(t) for t in os.environ.get("TETS", "32,64,128,256,384,768").split(",")]:
     up = torch.rand(p.packed_numel(T), dtype=torch.float64, device="cuda")
     fp = torch.zeros_like(up)
-    wp = torch.zeros_like(up)
+    wp = p.new_scratch(T)
     for _ in range(2):
         p.sweep_packed(up, fp, wp, T, 1)
     _lib.profile_enable(True)

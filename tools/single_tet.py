@@ -21,7 +21,7 @@ p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_ro
 N = lattice.interior_size(level)
 up = torch.rand(p.packed_numel(1), dtype=torch.float64, device="cuda")
 fp = torch.zeros_like(up)
-wp = torch.zeros_like(up)
+wp = p.new_scratch(1)
 for _ in range(2):
     p.sweep_packed(up, fp, wp, 1, 1)
 torch.cuda.synchronize()
