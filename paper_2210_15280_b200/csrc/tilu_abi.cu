@@ -144,9 +144,10 @@ bool batch_ok(const tilu_plan_t *p)
     return !(p->flags & TILU_SCHED_SIMPLE) && p->dev.level <= 9 && p->dev.n >= 4 && p->bsched != nullptr;
 }
 
-// Tets per lane of the packed layout (groups of 32 * tpl tets).  Two tets per lane halve the
-// per-point bookkeeping (dependency checks, tables, band lookups) per DoF once there are enough
-// tets to keep the groups' layer pipelines filled.  TILU_TPL=1|2 overrides (measurement only).
+// Tets per lane of the packed layout (groups of 32 * tpl tets).  More tets per lane amortise the
+// per-point bookkeeping and, above all, every producer -> consumer handoff between rows over more
+// DoF, once there are enough tets to keep the groups filled (T = 4 measured slower: register
+// spills, fewer warps).  TILU_TPL=1|2 overrides (measurement only).
 int batch_tpl(int ntets)
 {
     static const char *e = std::getenv("TILU_TPL");

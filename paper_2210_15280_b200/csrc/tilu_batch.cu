@@ -38,7 +38,7 @@ namespace tilu {
 constexpr int kWarps = 4;  // warps per CTA (independent; the CTA is only an occupancy unit)
 constexpr long long kSent = 0x7FF4DEADBEEF0001ll;  // signalling NaN: "not yet computed"
 
-// T tets per lane (T = 1: groups of 32 tets; T = 2: groups of 64, one 16-byte access per lane).
+// T tets per lane (T = 1, 2, 4: groups of 32, 64, 128 tets; T / 2 16-byte accesses per lane).
 template <int T>
 struct Vt {
     double a[T];
@@ -50,9 +50,12 @@ __device__ __forceinline__ Vt<T> ldv(const double *p)
     if constexpr (T == 1) {
         r.a[0] = *p;
     } else {
-        const double2 d = *reinterpret_cast<const double2 *>(p);
-        r.a[0] = d.x;
-        r.a[1] = d.y;
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) {
+            const double2 d = reinterpret_cast<const double2 *>(p)[i];
+            r.a[2 * i] = d.x;
+            r.a[2 * i + 1] = d.y;
+        }
     }
     return r;
 }
@@ -63,25 +66,26 @@ __device__ __forceinline__ Vt<T> ldcgv(const double *p)
     if constexpr (T == 1) {
         r.a[0] = __ldcg(p);
     } else {
-        const double2 d = __ldcg(reinterpret_cast<const double2 *>(p));
-        r.a[0] = d.x;
-        r.a[1] = d.y;
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) {
+            const double2 d = __ldcg(reinterpret_cast<const double2 *>(p) + i);
+            r.a[2 * i] = d.x;
+            r.a[2 * i + 1] = d.y;
+        }
     }
     return r;
 }
 template <int T>
 __device__ __forceinline__ void stv(double *p, const Vt<T> &v)
 {
-    if constexpr (T == 1) *p = v.a[0];
-    else *reinterpret_cast<double2 *>(p) = make_double2(v.a[0], v.a[1]);
+    if constexpr (T == 1) {
+        *p = v.a[0];
+    } else {
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) reinterpret_cast<double2 *>(p)[i] = make_double2(v.a[2 * i], v.a[2 * i + 1]);
+    }
 }
 
-// Warp-wide wait until *flag >= need (flag in shared or global memory).  Only lane 0 polls; the
-// warp then reconverges through __syncwarp(), which also orders lane 0's acquire before every
-// lane's subsequent loads.  (Letting all lanes poll is unsafe under independent thread scheduling:
-// lanes can leave the loop at different times while the compiler keeps the warp-uniform row
-// index in a uniform register -- observed as an out-of-range shared access.)  A dependency bug
-// must fail loudly, not hang the device: after ~10 s of polling the kernel traps.
 __device__ __forceinline__ bool is_sent(double v) { return __double_as_longlong(v) == kSent; }
 template <int T>
 __device__ __forceinline__ bool any_sent(const Vt<T> &v)
@@ -103,6 +107,62 @@ __device__ __forceinline__ Vt<T> sent_v()
 // Wait until no lane of the warp holds the sentinel in v (re-reading p from L2).  Warp-uniform
 // loop (__any_sync), so lanes never diverge around it; a dependency bug must fail loudly, not hang
 // the device: after ~2^26 re-reads the kernel traps.
+// ---- TMA bulk copies into a per-warp shared-memory ring (mbarrier completion) ----------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+template <int T>
+__device__ __forceinline__ Vt<T> ldsv(const double *p)
+{
+    return ldv<T>(p);
+}
+
+// Per-warp ring of D stages.  Stage = NS streams of one point (GW doubles each) + 8 coefficient
+// doubles (TAB).  Lane 0 issues the bulk copies of point p; every lane waits on the stage's
+// mbarrier and reads its own T values.  Issue and consume run in the same order through one
+// sequence counter per warp (stage = seq % D, parity = (seq / D) & 1).
+template <int NS, int GW, int D>
+struct Ring {
+    static constexpr int SD = NS * GW + 8;  // doubles per stage
+    double *buf;
+    uint64_t *mb;
+    uint32_t iss, con;
+    __device__ __forceinline__ double *stage(uint32_t seq) const { return buf + (seq % D) * SD; }
+};
+
+#ifdef TILU_STATS
+__device__ unsigned long long g_stats[4];  // [0] points, [1] points that found a sentinel, [2] re-reads
+#define TILU_STAT(i, v) (lane == 0 ? (void)atomicAdd(&g_stats[i], (unsigned long long)(v)) : (void)0)
+#else
+#define TILU_STAT(i, v) ((void)0)
+#endif
+
 template <int T>
 __device__ __forceinline__ void ready(Vt<T> &v, const double *p)
 {
@@ -112,6 +172,9 @@ __device__ __forceinline__ void ready(Vt<T> &v, const double *p)
         v = ldcgv<T>(p);
         if (++spins > (1ll << 26)) __trap();
     }
+#ifdef TILU_STATS
+    if ((threadIdx.x & 31) == 0 && spins) atomicAdd(&g_stats[2], (unsigned long long)spins);
+#endif
 }
 
 __device__ __forceinline__ bool in_band_b(int x, int y, int z, int xe) { return z == 1 || y == 1 || x == 1 || x == xe; }
@@ -229,16 +292,35 @@ __device__ __forceinline__ void fwd_band_load(double &dst, const PlanDev &P, con
     }
 }
 
+// Shared memory of the forward / backward kernels: per warp, D mbarriers + D ring stages.
+template <int NS, int T, int D>
+constexpr size_t ring_smem() { return (size_t)kWarps * D * (8 + (NS * 32 * T + 8) * 8); }
+template <int T>
+constexpr int kStages = T == 4 ? 2 : 4;  // ring depth (points in flight per warp)
+constexpr int kFwdNS = 8;    // forward ring streams: ue us un ubn ubc uts utc f
+constexpr int kBwdNS = 2;    // backward ring streams: w_f(p), u(p)
+
 template <int K, bool EXACT, bool CONST_ROW, int T, bool TAB>
-__global__ void __launch_bounds__(kWarps * 32, 4 / T) k_batch_fwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_batch_fwd(PlanDev P, BatchArgs A)
 {
-    constexpr uint32_t GW = 32u * T;
+    constexpr int GW = 32 * T, D = kStages<T>, NS = kFwdNS;
+    using RingT = Ring<NS, GW, D>;
+    extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_tab[kWarps][7 * K];
     __shared__ double s_L[kWarps][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n = P.n;
     const int total = P.nrows * A.G;
     double *tab = s_tab[warp];
     double *sL = s_L[warp];
+    RingT ring;
+    ring.mb = reinterpret_cast<uint64_t *>(smem) + warp * D;
+    ring.buf = reinterpret_cast<double *>(smem + (size_t)kWarps * D * 8) + (size_t)warp * D * RingT::SD;
+    ring.iss = ring.con = 0;
+    if (lane == 0) {
+        for (int i = 0; i < D; ++i) mbar_init(&ring.mb[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
     for (;;) {
         int tk = 0;
         if (lane == 0) tk = atomicAdd(A.ticket, 1);
@@ -248,11 +330,11 @@ __global__ void __launch_bounds__(kWarps * 32, 4 / T) k_batch_fwd(PlanDev P, Bat
         const int ri = tk / A.G, g = tk - ri * A.G;
         const int zy = P.order[ri], z = zy >> 10, y = zy & 1023;
         TILU_CHECK(y >= 1 && z >= 1 && y + z <= n - 2, "fwd row", y, z);
-        const size_t gbase = (size_t)g * P.grid * GW + (size_t)lane * T;
-        const double *__restrict__ u = A.u + gbase;
-        const double *__restrict__ f = A.f + gbase;
-        double *wa = A.wa + gbase;
-        double *wb = A.wb + gbase;
+        const size_t gb0 = (size_t)g * P.grid * GW;
+        const double *ug = A.u + gb0, *fg = A.f + gb0;  // group bases (bulk copies)
+        const double *__restrict__ u = ug + lane * T;
+        double *wa = A.wa + gb0 + lane * T;
+        double *wb = A.wb + gb0 + lane * T;
         FwdRow R;
         R.y = y;
         R.m = n - 1 - z - y;
@@ -267,8 +349,29 @@ __global__ void __launch_bounds__(kWarps * 32, 4 / T) k_batch_fwd(PlanDev P, Bat
         R.boff = P.variant == 1 ? P.bandoff[R.rid] : 0;
         const int m = R.m;
         const double *cf = P.coefF + 8 * ((int64_t)(R.oc / GW));  // TAB: coefficients of (0, y, z)
+        // ring producer: point p's u/f segments (+ coefficients) into the next stage
+        auto issue = [&](int p) {
+            if (lane == 0) {
+                const uint32_t X = (uint32_t)p * GW, B = GW * 8;
+                double *st = ring.stage(ring.iss);
+                uint64_t *mb = &ring.mb[ring.iss % D];
+                mbar_expect_tx(mb, NS * B + (TAB ? 64u : 0u));
+                bulk_g2s(st + 0 * GW, ug + R.oc + X + GW, B, mb);   // ue
+                bulk_g2s(st + 1 * GW, ug + R.os + X + GW, B, mb);   // us
+                bulk_g2s(st + 2 * GW, ug + R.on + X, B, mb);        // un
+                bulk_g2s(st + 3 * GW, ug + R.obn + X, B, mb);       // ubn
+                bulk_g2s(st + 4 * GW, ug + R.obc + X + GW, B, mb);  // ubc
+                bulk_g2s(st + 5 * GW, ug + R.ots + X + GW, B, mb);  // uts
+                bulk_g2s(st + 6 * GW, ug + R.otc + X, B, mb);       // utc
+                bulk_g2s(st + 7 * GW, fg + R.oc + X, B, mb);        // f
+                if (TAB) bulk_g2s(st + NS * GW, cf + 8 * p, 64, mb);
+            }
+            ++ring.iss;
+        };
+        __syncwarp();  // every lane is done with the stages about to be refilled
+        for (int p = 1; p <= min(D, m); ++p) issue(p);
         if constexpr (!TAB) smem_load_table<7, K>(tab, P.seedF + (int64_t)R.rid * 7 * K, lane);
-        // sliding windows (values of point x-1 / x that point x+1 reuses) and point 1
+        // sliding windows (values of point x-1 / x that point x+1 reuses)
         Vt<T> u_wm = ldv<T>(u + R.oc), u_c = ldv<T>(u + R.oc + GW), us0 = ldv<T>(u + R.os + GW);
         Vt<T> un_m = ldv<T>(u + R.on), ubn_m = ldv<T>(u + R.obn), ubc0 = ldv<T>(u + R.obc + GW);
         Vt<T> uts0 = ldv<T>(u + R.ots + GW), utc_m = ldv<T>(u + R.otc);
@@ -278,41 +381,46 @@ __global__ void __launch_bounds__(kWarps * 32, 4 / T) k_batch_fwd(PlanDev P, Bat
         for (int t = 0; t < T; ++t) wprev.a[t] = ss.a[t] = 0.0;
         ready<T>(ws0, wa + R.os + GW);
         ready<T>(wbc0, wa + R.obc + GW);
-        FwdSlot<T> C, N;
-        fwd_load<T>(C, u, f, wa, R, 1);
+        // neighbours' w (produced concurrently): direct L2 loads one point ahead (generic 8 / 16-byte
+        // loads: single-copy atomic per double, which the sentinel protocol relies on; prefetching
+        // further ahead mostly finds sentinels -- the rows run a few points behind their producers)
+        Vt<T> ws = ldcgv<T>(wa + R.os + 2 * GW), wbn = ldcgv<T>(wa + R.obn + GW), wbc = ldcgv<T>(wa + R.obc + 2 * GW);
         double cband = 0.0, nband = 0.0;
-        double Lc[8], Ln[8];
-        if constexpr (TAB) ld_coef(Lc, cf + 8);
-        else fwd_band_load(cband, P, R, z, 1, lane);
+        if constexpr (!TAB) fwd_band_load(cband, P, R, z, 1, lane);
         for (int x = 1; x <= m; ++x) {
-            const int pn = min(x + 1, m);  // prefetch (at the row end: re-read point m, unused)
-            fwd_load<T>(N, u, f, wa, R, pn);
-            if constexpr (TAB) ld_coef(Ln, cf + 8 * pn);
-            else fwd_band_load(nband, P, R, z, pn, lane);
-            // stencil row: constant -> kernel-parameter constant bank operands (indices are
-            // compile-time after unrolling; never take the parameter's address: that copies it
-            // to local memory), else the per-point rows of P.arows
+            const uint32_t X = (uint32_t)x * GW;
+            const int pn = min(x + 1, m);  // (at the row end: re-read point m, unused)
+            const uint32_t XN = (uint32_t)pn * GW;
+            const Vt<T> ws_n = ldcgv<T>(wa + R.os + XN + GW), wbn_n = ldcgv<T>(wa + R.obn + XN),
+                        wbc_n = ldcgv<T>(wa + R.obc + XN + GW);
+            if constexpr (!TAB) fwd_band_load(nband, P, R, z, pn, lane);
             double a[15];
 #pragma unroll
             for (int i = 0; i < 15; ++i) a[i] = CONST_ROW ? A.arow[i] : P.arows[15 * (int64_t)(R.oc / GW + x) + i];
-            // L entries: from the coefficient table, or lane m publishes L_m (band store or the
-            // shared NDDF table)
+            // this point's u/f (and coefficients) from the ring
+            const double *st = ring.stage(ring.con);
+            mbar_wait(&ring.mb[ring.con % D], (ring.con / D) & 1);
+            ++ring.con;
+            const double *sl = st + lane * T;
+            const Vt<T> ue = ldsv<T>(sl + 0 * GW), us = ldsv<T>(sl + 1 * GW), un = ldsv<T>(sl + 2 * GW);
+            const Vt<T> ubn = ldsv<T>(sl + 3 * GW), ubc = ldsv<T>(sl + 4 * GW), uts = ldsv<T>(sl + 5 * GW);
+            const Vt<T> utc = ldsv<T>(sl + 6 * GW), fv = ldsv<T>(sl + 7 * GW);
             double L[7];
             if constexpr (TAB) {
 #pragma unroll
-                for (int i = 0; i < 7; ++i) L[i] = Lc[i];
+                for (int i = 0; i < 7; ++i) L[i] = st[NS * GW + i];
             } else {
                 if (lane < 7) sL[lane] = (P.variant == 1 && in_band_b(x, y, z, m)) ? cband : tab[lane * K];
                 __syncwarp();
 #pragma unroll
                 for (int i = 0; i < 7; ++i) L[i] = sL[i];
             }
-            // neighbours' w of point x: final unless still the sentinel (then wait)
-            if (__any_sync(0xffffffffu, any_sent(C.ws) | any_sent(C.wbn) | any_sent(C.wbc))) {
-                const uint32_t X = (uint32_t)x * GW;
-                ready<T>(C.ws, wa + R.os + X + GW);
-                ready<T>(C.wbn, wa + R.obn + X);
-                ready<T>(C.wbc, wa + R.obc + X + GW);
+            TILU_STAT(0, 1);
+            if (__any_sync(0xffffffffu, any_sent(ws) | any_sent(wbn) | any_sent(wbc))) {
+                TILU_STAT(1, 1);
+                ready<T>(ws, wa + R.os + X + GW);
+                ready<T>(wbn, wa + R.obn + X);
+                ready<T>(wbc, wa + R.obc + X + GW);
             }
             Vt<T> v;
 #pragma unroll
@@ -321,61 +429,61 @@ __global__ void __launch_bounds__(kWarps * 32, 4 / T) k_batch_fwd(PlanDev P, Bat
                 double acc = EXACT ? dmul(a[7], u_c.a[t]) : a[7] * u_c.a[t];
                 acc = madd<EXACT>(acc, a[0], u_wm.a[t]);
                 acc = madd<EXACT>(acc, a[1], us0.a[t]);
-                acc = madd<EXACT>(acc, a[2], C.us.a[t]);
+                acc = madd<EXACT>(acc, a[2], us.a[t]);
                 acc = madd<EXACT>(acc, a[3], ubn_m.a[t]);
-                acc = madd<EXACT>(acc, a[4], C.ubn.a[t]);
+                acc = madd<EXACT>(acc, a[4], ubn.a[t]);
                 acc = madd<EXACT>(acc, a[5], ubc0.a[t]);
-                acc = madd<EXACT>(acc, a[6], C.ubc.a[t]);
-                acc = madd<EXACT>(acc, a[8], C.ue.a[t]);
-                acc = madd<EXACT>(acc, a[9], C.un.a[t]);
+                acc = madd<EXACT>(acc, a[6], ubc.a[t]);
+                acc = madd<EXACT>(acc, a[8], ue.a[t]);
+                acc = madd<EXACT>(acc, a[9], un.a[t]);
                 acc = madd<EXACT>(acc, a[10], un_m.a[t]);
-                acc = madd<EXACT>(acc, a[11], C.uts.a[t]);
+                acc = madd<EXACT>(acc, a[11], uts.a[t]);
                 acc = madd<EXACT>(acc, a[12], uts0.a[t]);
-                acc = madd<EXACT>(acc, a[13], C.utc.a[t]);
+                acc = madd<EXACT>(acc, a[13], utc.a[t]);
                 acc = madd<EXACT>(acc, a[14], utc_m.a[t]);
-                const double r = dsub(C.f.a[t], acc);
+                const double r = dsub(fv.a[t], acc);
                 ss.a[t] = fma(r, r, ss.a[t]);
                 double vv;
                 if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
                     vv = msub<true>(r, L[0], wprev.a[t]);
                     vv = msub<true>(vv, L[1], ws0.a[t]);
-                    vv = msub<true>(vv, L[2], C.ws.a[t]);
+                    vv = msub<true>(vv, L[2], ws.a[t]);
                     vv = msub<true>(vv, L[3], wbn_m.a[t]);
-                    vv = msub<true>(vv, L[4], C.wbn.a[t]);
+                    vv = msub<true>(vv, L[4], wbn.a[t]);
                     vv = msub<true>(vv, L[5], wbc0.a[t]);
-                    vv = msub<true>(vv, L[6], C.wbc.a[t]);
+                    vv = msub<true>(vv, L[6], wbc.a[t]);
                 } else {  // own-row term last: one FMA on the row's dependency chain
                     vv = msub<false>(r, L[1], ws0.a[t]);
-                    vv = msub<false>(vv, L[2], C.ws.a[t]);
+                    vv = msub<false>(vv, L[2], ws.a[t]);
                     vv = msub<false>(vv, L[3], wbn_m.a[t]);
-                    vv = msub<false>(vv, L[4], C.wbn.a[t]);
+                    vv = msub<false>(vv, L[4], wbn.a[t]);
                     vv = msub<false>(vv, L[5], wbc0.a[t]);
-                    vv = msub<false>(vv, L[6], C.wbc.a[t]);
+                    vv = msub<false>(vv, L[6], wbc.a[t]);
                     vv = msub<false>(vv, L[0], wprev.a[t]);
                 }
                 v.a[t] = vv;
             }
-            stv<T>(wa + R.oc + (uint32_t)x * GW, v);
-            stv<T>(wb + R.oc + (uint32_t)x * GW, sent_v<T>());  // re-arm w_b for the backward pass
+            stv<T>(wa + R.oc + X, v);
+            stv<T>(wb + R.oc + X, sent_v<T>());  // re-arm w_b for the backward pass
             if constexpr (!TAB) smem_march<7, K>(tab, lane);
+            __syncwarp();  // every lane has read this stage: it may be refilled
+            if (x + D <= m) issue(x + D);
             u_wm = u_c;
-            u_c = C.ue;
-            us0 = C.us;
-            un_m = C.un;
-            ubn_m = C.ubn;
-            ubc0 = C.ubc;
-            uts0 = C.uts;
-            utc_m = C.utc;
-            ws0 = C.ws;
-            wbn_m = C.wbn;
-            wbc0 = C.wbc;
+            u_c = ue;
+            us0 = us;
+            un_m = un;
+            ubn_m = ubn;
+            ubc0 = ubc;
+            uts0 = uts;
+            utc_m = utc;
+            ws0 = ws;
+            wbn_m = wbn;
+            wbc0 = wbc;
+            ws = ws_n;
+            wbn = wbn_n;
+            wbc = wbc_n;
             wprev = v;
-            C = N;
             cband = nband;
-            if constexpr (TAB) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) Lc[i] = Ln[i];
-            }
         }
         if (A.part) {
 #pragma unroll
@@ -439,15 +547,26 @@ __device__ __forceinline__ int bwd_band_load(double &dst, const BwdRow &R, const
 }
 
 template <int K, bool EXACT, int T, bool TAB>
-__global__ void __launch_bounds__(kWarps * 32, 4 / T) k_batch_bwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_batch_bwd(PlanDev P, BatchArgs A)
 {
-    constexpr uint32_t GW = 32u * T;
+    constexpr int GW = 32 * T, D = kStages<T>, NS = kBwdNS;
+    using RingT = Ring<NS, GW, D>;
+    extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_tab[kWarps][8 * K];
     __shared__ double s_L[kWarps][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n = P.n;
     const int total = P.nrows * A.G;
     double *tab = s_tab[warp];
     double *sL = s_L[warp];
+    RingT ring;
+    ring.mb = reinterpret_cast<uint64_t *>(smem) + warp * D;
+    ring.buf = reinterpret_cast<double *>(smem + (size_t)kWarps * D * 8) + (size_t)warp * D * RingT::SD;
+    ring.iss = ring.con = 0;
+    if (lane == 0) {
+        for (int i = 0; i < D; ++i) mbar_init(&ring.mb[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
     for (;;) {
         int tk = 0;
         if (lane == 0) tk = atomicAdd(A.ticket, 1);
@@ -456,10 +575,11 @@ __global__ void __launch_bounds__(kWarps * 32, 4 / T) k_batch_bwd(PlanDev P, Bat
         const int rr = tk / A.G, g = tk - rr * A.G, ri = P.nrows - 1 - rr;
         const int zy = P.order[ri], z = zy >> 10, y = zy & 1023;
         TILU_CHECK(y >= 1 && z >= 1 && y + z <= n - 2, "bwd row", y, z);
-        const size_t gbase = (size_t)g * P.grid * GW + (size_t)lane * T;
-        double *__restrict__ u = A.u + gbase;
-        double *wa = A.wa + gbase;
-        double *wb = A.wb + gbase;
+        const size_t gb0 = (size_t)g * P.grid * GW;
+        const double *ug = A.u + gb0, *wag = A.wa + gb0;  // group bases (bulk copies)
+        double *__restrict__ u = A.u + gb0 + lane * T;
+        double *wa = A.wa + gb0 + lane * T;
+        double *wb = A.wb + gb0 + lane * T;
         BwdRow R;
         R.y = y;
         R.m = n - 1 - z - y;
@@ -470,6 +590,21 @@ __global__ void __launch_bounds__(kWarps * 32, 4 / T) k_batch_bwd(PlanDev P, Bat
         R.otc = (uint32_t)row_offset(n, z + 1, y) * GW;
         const int m = R.m;
         const double *cb = P.coefB + 8 * ((int64_t)(R.oc / GW));  // TAB: coefficients of (0, y, z)
+        // ring producer: point x's own w_f and u (+ coefficients); points in descending x
+        auto issue = [&](int x) {
+            if (lane == 0) {
+                const uint32_t X = (uint32_t)x * GW, B = GW * 8;
+                double *st = ring.stage(ring.iss);
+                uint64_t *mb = &ring.mb[ring.iss % D];
+                mbar_expect_tx(mb, NS * B + (TAB ? 64u : 0u));
+                bulk_g2s(st + 0 * GW, wag + R.oc + X, B, mb);  // w_f(p): final since the forward pass
+                bulk_g2s(st + 1 * GW, ug + R.oc + X, B, mb);   // u(p)
+                if (TAB) bulk_g2s(st + NS * GW, cb + 8 * x, 64, mb);
+            }
+            ++ring.iss;
+        };
+        __syncwarp();  // every lane is done with the stages about to be refilled
+        for (int k = 1; k <= min(D, m); ++k) issue(m - k + 1);
         if (!TAB && lane < 8) {  // the row of q_m (lane m) or the own row (lane 7)
             const int qy = lane < 7 ? y - kDY[lane] : y, qz = lane < 7 ? z - kDZ[lane] : z;
             const bool valid = qy >= 1 && qz >= 1 && qy + qz <= n - 2;
@@ -484,75 +619,80 @@ __global__ void __launch_bounds__(kWarps * 32, 4 / T) k_batch_bwd(PlanDev P, Bat
         Vt<T> wprev;
 #pragma unroll
         for (int t = 0; t < T; ++t) wprev.a[t] = 0.0;
-        BwdSlot<T> C, N;
-        bwd_load<T>(C, u, wa, wb, R, m);
+        // neighbours' w_b (produced concurrently): direct L2 loads, one point ahead
+        Vt<T> wn = ldcgv<T>(wb + R.on + M - GW), wts = ldcgv<T>(wb + R.ots + M), wtc = ldcgv<T>(wb + R.otc + M - GW);
         double cband = 0.0, nband = 0.0;
-        double Lc[8], Ln[8];
         int csrc = 2, nsrc = 2;
-        if constexpr (TAB) ld_coef(Lc, cb + 8 * m);
-        else csrc = bwd_band_load(cband, R, P, n, z, m, lane);
+        if constexpr (!TAB) csrc = bwd_band_load(cband, R, P, n, z, m, lane);
         for (int k = 1; k <= m; ++k) {
             const int x = m - k + 1;
-            const int xn = max(x - 1, 1);  // prefetch the next point (at the row end: re-read x = 1)
-            bwd_load<T>(N, u, wa, wb, R, xn);
-            if constexpr (TAB) ld_coef(Ln, cb + 8 * xn);
-            else nsrc = bwd_band_load(nband, R, P, n, z, xn, lane);
+            const uint32_t X = (uint32_t)x * GW;
+            const int xn = max(x - 1, 1);  // (at the row end: re-read x = 1, unused)
+            const uint32_t XN = (uint32_t)xn * GW;
+            const Vt<T> wn_n = ldcgv<T>(wb + R.on + XN - GW), wts_n = ldcgv<T>(wb + R.ots + XN),
+                        wtc_n = ldcgv<T>(wb + R.otc + XN - GW);
+            if constexpr (!TAB) nsrc = bwd_band_load(nband, R, P, n, z, xn, lane);
+            const double *st = ring.stage(ring.con);
+            mbar_wait(&ring.mb[ring.con % D], (ring.con / D) & 1);
+            ++ring.con;
+            const Vt<T> wf = ldsv<T>(st + lane * T), uo = ldsv<T>(st + GW + lane * T);
             double L[8];
             if constexpr (TAB) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) L[i] = Lc[i];
+                for (int i = 0; i < 8; ++i) L[i] = st[NS * GW + i];
             } else {
                 if (lane < 8) sL[lane] = csrc == 0 ? 0.0 : (csrc == 1 ? cband : tab[lane * K]);
                 __syncwarp();
 #pragma unroll
                 for (int i = 0; i < 8; ++i) L[i] = sL[i];
             }
-            const uint32_t X = (uint32_t)x * GW;
-            if (__any_sync(0xffffffffu, any_sent(C.wn) | any_sent(C.wts) | any_sent(C.wtc))) {
-                ready<T>(C.wn, wb + R.on + X - GW);
-                ready<T>(C.wts, wb + R.ots + X);
-                ready<T>(C.wtc, wb + R.otc + X - GW);
+            TILU_STAT(0, 1);
+            if (__any_sync(0xffffffffu, any_sent(wn) | any_sent(wts) | any_sent(wtc))) {
+                TILU_STAT(1, 1);
+                ready<T>(wn, wb + R.on + X - GW);
+                ready<T>(wts, wb + R.ots + X);
+                ready<T>(wtc, wb + R.otc + X - GW);
             }
             const double inv_d = L[7];
             Vt<T> v, un;
 #pragma unroll
             for (int t = 0; t < T; ++t) {
-                double vv = EXACT ? dmul(inv_d, C.wf.a[t]) : inv_d * C.wf.a[t];
+                double vv = EXACT ? dmul(inv_d, wf.a[t]) : inv_d * wf.a[t];
                 if (EXACT) {  // reference order (_kernels.py:404-425)
                     vv = msub<true>(vv, L[0], wprev.a[t]);
                     vv = msub<true>(vv, L[1], wn_hi.a[t]);
-                    vv = msub<true>(vv, L[2], C.wn.a[t]);
+                    vv = msub<true>(vv, L[2], wn.a[t]);
                     vv = msub<true>(vv, L[3], wts_hi.a[t]);
-                    vv = msub<true>(vv, L[4], C.wts.a[t]);
+                    vv = msub<true>(vv, L[4], wts.a[t]);
                     vv = msub<true>(vv, L[5], wtc_hi.a[t]);
-                    vv = msub<true>(vv, L[6], C.wtc.a[t]);
+                    vv = msub<true>(vv, L[6], wtc.a[t]);
                 } else {
                     vv = msub<false>(vv, L[1], wn_hi.a[t]);
-                    vv = msub<false>(vv, L[2], C.wn.a[t]);
+                    vv = msub<false>(vv, L[2], wn.a[t]);
                     vv = msub<false>(vv, L[3], wts_hi.a[t]);
-                    vv = msub<false>(vv, L[4], C.wts.a[t]);
+                    vv = msub<false>(vv, L[4], wts.a[t]);
                     vv = msub<false>(vv, L[5], wtc_hi.a[t]);
-                    vv = msub<false>(vv, L[6], C.wtc.a[t]);
+                    vv = msub<false>(vv, L[6], wtc.a[t]);
                     vv = msub<false>(vv, L[0], wprev.a[t]);
                 }
                 v.a[t] = vv;
-                un.a[t] = dadd(C.u.a[t], vv);
+                un.a[t] = dadd(uo.a[t], vv);
             }
             stv<T>(wb + R.oc + X, v);
             stv<T>(u + R.oc + X, un);
             stv<T>(wa + R.oc + X, sent_v<T>());  // re-arm w_f for the next forward pass
             if constexpr (!TAB) smem_march<8, K>(tab, lane);
-            wn_hi = C.wn;
-            wts_hi = C.wts;
-            wtc_hi = C.wtc;
+            __syncwarp();  // every lane has read this stage: it may be refilled
+            if (k + D <= m) issue(m - (k + D) + 1);
+            wn_hi = wn;
+            wts_hi = wts;
+            wtc_hi = wtc;
+            wn = wn_n;
+            wts = wts_n;
+            wtc = wtc_n;
             wprev = v;
-            C = N;
             cband = nband;
             csrc = nsrc;
-            if constexpr (TAB) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) Lc[i] = Ln[i];
-            }
         }
     }
     // the last warp to finish marks the scratch ready (w_f re-armed everywhere) for the next call
@@ -712,6 +852,15 @@ __global__ void k_batch_norms(const double *__restrict__ part, int nrows, int nt
 // padded 32-tet blocks: all blocks of the last group are written (zeros for tets >= ntets)
 static unsigned tet_blocks(int ntets, int tpl) { return (unsigned)(((ntets + 32 * tpl - 1) / (32 * tpl)) * tpl); }
 
+#ifdef TILU_STATS
+extern "C" void tilu_stats_read(unsigned long long *out)
+{
+    cudaMemcpyFromSymbol(out, g_stats, sizeof(g_stats));
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_stats, z, sizeof(z));
+}
+#endif
+
 void launch_pack(const double *src, double *dst, int64_t grid, int ntets, int tpl, cudaStream_t s)
 {
     dim3 gr((unsigned)((grid + 31) / 32), tet_blocks(ntets, tpl));
@@ -739,22 +888,24 @@ void launch_arm(const PlanDev &P, double *wa, const unsigned long long *hdr, uns
 
 // Persistent grid: as many CTAs as fit on the device at once (queried once per kernel).
 template <class Kern>
-static unsigned persistent_grid(Kern k)
+static unsigned persistent_grid(Kern k, size_t smem)
 {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kWarps * 32, 0);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kWarps * 32, smem);
     return (unsigned)std::max(1, sms * std::max(per, 1));
 }
 
 template <int K, int T, bool TAB>
 static void launch_fwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_t s)
 {
+    constexpr size_t sm = ring_smem<kFwdNS, T, kStages<T>>();
     auto run = [&](auto kern) {
-        static const unsigned grid = persistent_grid(kern);
+        static const unsigned grid = persistent_grid(kern, sm);
         A.nwarps = (int)grid * kWarps;
-        kern<<<grid, kWarps * 32, 0, s>>>(P, A);
+        kern<<<grid, kWarps * 32, sm, s>>>(P, A);
     };
     const bool c = P.arow != nullptr;
     if (exact) {
@@ -769,10 +920,11 @@ static void launch_fwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_
 template <int K, int T, bool TAB>
 static void launch_bwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_t s)
 {
+    constexpr size_t sm = ring_smem<kBwdNS, T, kStages<T>>();
     auto run = [&](auto kern) {
-        static const unsigned grid = persistent_grid(kern);
+        static const unsigned grid = persistent_grid(kern, sm);
         A.nwarps = (int)grid * kWarps;
-        kern<<<grid, kWarps * 32, 0, s>>>(P, A);
+        kern<<<grid, kWarps * 32, sm, s>>>(P, A);
     };
     if (exact) run(k_batch_bwd<K, true, T, TAB>);
     else run(k_batch_bwd<K, false, T, TAB>);

@@ -251,6 +251,28 @@ def test_packed_resident_api_and_roundtrip():
     assert torch.equal(back, ref)
 
 
+@pytest.mark.parametrize("T", [3, 70])
+def test_packed_scratch_state_across_calls(T):
+    """The scratch keeps the sentinel-armed work vectors across calls: k single-sweep calls equal one
+    k-sweep call bitwise, and a clobbered scratch (header no longer matching) is re-armed."""
+    level, q = 5, 5
+    src, fit, u0 = _oracle_case(level, q, verts=lattice.kuhn_tet((2, 1, 0)))
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data)
+    rng = np.random.default_rng(T)
+    us = cuda(np.stack([u0 * s for s in rng.uniform(0.5, 2.0, T)]))
+    fs = cuda(rng.standard_normal(us.shape) * lattice.interior_mask(level))
+    up1, up3, fp = p.pack(us), p.pack(us), p.pack(fs)
+    w1, w3 = p.new_scratch(T), p.new_scratch(T)
+    for _ in range(3):
+        p.sweep_packed(up1, fp, w1, T, 1)
+    p.sweep_packed(up3, fp, w3, T, 3)
+    assert torch.equal(up1, up3)
+    w1.fill_(1.0)                              # clobber: values, boundary and header
+    p.sweep_packed(up1, fp, w1, T, 1)
+    p.sweep_packed(up3, fp, w3, T, 1)
+    assert torch.equal(up1, up3)
+
+
 def test_packed_fast_mode_within_1e12():
     level, q, T = 6, 6, 5
     src, fit, u0 = _oracle_case(level, q, verts=lattice.kuhn_tet((1, 2, 0)))
