@@ -80,55 +80,66 @@ class Dist:
 # clocks sampler (nvidia-smi during the timed region)
 # ----------------------------------------------------------------------------------------------
 class Clocks:
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled DURING the timed region: NVML (pynvml) every 2 ms on a
+    side thread (short timed regions still get samples); nvidia-smi -lms fallback."""
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.lines: list[str] = []
-        self.proc = None
+        self.sm: list[float] = []
+        self.smax: list[float] = []
+        self.mask = 0
+        self.stop_ev = threading.Event()
+        self.t = None
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            try:
+                import torch
+                uuid = str(torch.cuda.get_device_properties(gpu).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+            self.nvml, self.h = pynvml, h
+        except Exception:
+            self.nvml = None
+
+    def _sample(self):
+        N, h = self.nvml, self.h
+        self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+        self.smax.append(float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)))
+        try:
+            self.mask |= int(N.nvmlDeviceGetCurrentClocksEventReasons(h))
+        except AttributeError:
+            self.mask |= int(N.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            self.stop_ev.wait(0.002)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except (FileNotFoundError, OSError):
-            self.proc = None
+        if self.nvml is None:
             return
-        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+        if self.nvml is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self.stop_ev.set()
         self.t.join(timeout=2)
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                smax.append(float(f[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.sm:
+            self._sample()
+        reasons = sorted(k for k, bit in self.REASONS.items() if self.mask & bit)
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.smax), "reasons": reasons,
+                "samples": len(self.sm), "source": "NVML, 2 ms period, timed region"}
 
 
 # ----------------------------------------------------------------------------------------------
@@ -159,7 +170,9 @@ def algo_bytes(level: int, nband: int, variant: str, shared_surrogate: bool = Tr
     """Algorithmic bytes per interior DoF.  "sweep" is SURVEY 8(d)'s fixed model (vectors once per
     pass, plus each tet's V1 band rows once per pass).  The per-kernel figures count what a kernel
     must move: the batched kernels share ONE band store among all tets of a group (read once per
-    layer CTA, L2-resident), so their per-DoF band share is ~0."""
+    point, through the per-point coefficient table shared by every tet of the batch, L2-resident),
+    so their per-DoF band share is ~0; the sentinel re-arm writes (8 B/DoF per pass) are an
+    implementation overhead and are not counted."""
     from paper_2210_15280_b200 import lattice
     N = lattice.interior_size(level)
     band = 72.0 * nband / N if variant == "v1" else 0.0
@@ -336,14 +349,14 @@ def run_ours(args, D: Dist):
     if args.e2e_sweeps > 0:
         uh = torch.from_numpy(u_host).pin_memory()
         fh = torch.zeros_like(uh).pin_memory()
-        mm.apply_host(uh.clone().pin_memory(), fh, args.e2e_sweeps)  # warm
+        mm.apply_host(uh.clone().pin_memory(), fh, args.e2e_sweeps, chunk=args.e2e_chunk)  # warm
         torch.cuda.synchronize()
         D.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = max(1, min(args.steps, 3))
         e0.record()
         for _ in range(reps):
-            mm.apply_host(uh, fh, args.e2e_sweeps)
+            mm.apply_host(uh, fh, args.e2e_sweeps, chunk=args.e2e_chunk)
         e1.record()
         torch.cuda.synchronize()
         D.barrier()
@@ -353,7 +366,8 @@ def run_ours(args, D: Dist):
         e2e = {"value": dofs_total * args.e2e_sweeps / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d * D.world, "d2h_bytes_per_step": d2h * D.world,
                "sweeps_per_step": args.e2e_sweeps, "ms_per_step": ems,
-               "api": "MacroMeshSmoother.apply_host(pinned u, f, sweeps)"}
+               "api": f"MacroMeshSmoother.apply_host(pinned u, f, sweeps): {args.e2e_chunk}-tet chunks "
+                      f"pipelined on 2 streams (H2D / sweeps / D2H overlap)"}
 
     # CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -387,6 +401,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-sweeps", type=int, default=3)
+    ap.add_argument("--e2e-chunk", type=int, default=64, help="tets per pipelined host<->device chunk")
     ap.add_argument("--fast", action="store_true", help="FMA substitution (<=1e-12, not bitwise)")
     ap.add_argument("--simple", action="store_true", help="force the reference-layout kernels")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")

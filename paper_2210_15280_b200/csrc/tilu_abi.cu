@@ -30,7 +30,8 @@ bool launch_simple_solve(const PlanDev &P, bool exact, bool stored, double *w, d
                          int which, cudaStream_t s);
 void launch_pack(const double *src, double *dst, int64_t grid, int ntets, int tpl, cudaStream_t s);
 void launch_unpack(const double *src, double *dst, int64_t grid, int ntets, int tpl, cudaStream_t s);
-void launch_batch_norms(const double *part, int nl, int ntets, int tpl, double *out, cudaStream_t s);
+void launch_batch_norms(double *part, int nrows, int ntets, int tpl, double *out, cudaStream_t s);
+size_t norm_scratch_doubles(int G, int tpl);
 bool launch_batch_pass(const PlanDev &P, const BatchArgs &A, bool exact, bool fwd, cudaStream_t s);
 bool launch_coef_tables(const PlanDev &P, double *cf, double *cb, cudaStream_t s);
 void launch_arm(const PlanDev &P, double *wa, const unsigned long long *hdr, unsigned long long key, int G, int tpl,
@@ -226,7 +227,7 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *ws
     if (!want_tables(p, ntets)) PK.coefF = PK.coefB = nullptr;
     Scratch sc(s);
     int *sync = reinterpret_cast<int *>(sc.get(2));  // fwd ticket, bwd ticket, bwd done
-    double *part = rnorm2 ? sc.get((size_t)G * P.nrows * gw) : nullptr;
+    double *part = rnorm2 ? sc.get((size_t)G * P.nrows * gw + norm_scratch_doubles(G, tpl)) : nullptr;
     if (!sync || (rnorm2 && !part)) return fail(TILU_ENOMEM, "scratch allocation failed");
     const bool exact = !(p->flags & TILU_FAST);
     BatchArgs A{};
@@ -262,8 +263,10 @@ int packed_sweeps(const tilu_plan_t *p, double *up, const double *fp, double *ws
         if (!ok) return fail(TILU_EUNSUPPORTED, "kx+1 = %d not compiled", P.kx1);
         g_launches += 2;
         if (rnorm2) {
+            prof_begin(s);
             launch_batch_norms(part, P.nrows, ntets, tpl, rnorm2 + (int64_t)k * ntets, s);
-            ++g_launches;
+            prof_end("batch_norms", s);
+            g_launches += 2;
         }
     }
     return TILU_OK;

@@ -829,20 +829,41 @@ __global__ void __launch_bounds__(256) k_arm(PlanDev P, double *__restrict__ wa,
                                              unsigned long long key, int tpl)
 {
     if (*hdr == key) return;
-    const int rid = blockIdx.x, g = blockIdx.y, gw = 32 * tpl;
-    const int z = P.rows[rid].z, y = P.rows[rid].y, m = P.n - 1 - z - y;
-    double *p = wa + ((size_t)g * P.grid + row_offset(P.n, z, y) + 1) * gw;
-    for (int i = threadIdx.x; i < m * gw; i += blockDim.x) p[i] = __longlong_as_double(kSent);
+    const int g = blockIdx.y, gw = 32 * tpl;
+    for (int rid = blockIdx.x; rid < P.nrows; rid += gridDim.x) {
+        const int z = P.rows[rid].z, y = P.rows[rid].y, m = P.n - 1 - z - y;
+        double *p = wa + ((size_t)g * P.grid + row_offset(P.n, z, y) + 1) * gw;
+        for (int i = threadIdx.x; i < m * gw; i += blockDim.x) p[i] = __longlong_as_double(kSent);
+    }
 }
 
-// rnorm2[t] = sum over rows (wavefront order) of the forward kernel's per-row partials.
-__global__ void k_batch_norms(const double *__restrict__ part, int nrows, int ntets, int gw, double *__restrict__ out)
+// rnorm2[t] = sum over rows of the forward kernel's per-row partials [G][nrows][gw], in two
+// fixed-order levels (deterministic): block (b, g) sums row chunk b of group g -- thread (j, l) takes
+// rows j, j + J, ... of lane l (coalesced over l), the J sums are added in order -- into
+// mid[g][b][l]; then k_norms_final adds the kNormChunks chunk sums of each tet in order.
+constexpr int kNormChunks = 64;
+__global__ void __launch_bounds__(256) k_batch_norms(const double *__restrict__ part, int nrows, int gw,
+                                                     double *__restrict__ mid)
+{
+    __shared__ double red[256];
+    const int b = blockIdx.x, g = blockIdx.y, l = threadIdx.x % gw, j = threadIdx.x / gw, J = blockDim.x / gw;
+    const int per = (nrows + kNormChunks - 1) / kNormChunks, r0 = b * per, r1 = min(nrows, r0 + per);
+    double s = 0.0;
+    for (int r = r0 + j; r < r1; r += J) s += part[((int64_t)g * nrows + r) * gw + l];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (j == 0) {
+        for (int k = 1; k < J; ++k) s += red[k * gw + l];
+        mid[((int64_t)g * kNormChunks + b) * gw + l] = s;
+    }
+}
+__global__ void k_norms_final(const double *__restrict__ mid, int ntets, int gw, double *__restrict__ out)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntets) return;
     const int g = t / gw, l = t % gw;
     double s = 0.0;
-    for (int r = 0; r < nrows; ++r) s += part[((int64_t)g * nrows + r) * gw + l];
+    for (int b = 0; b < kNormChunks; ++b) s += mid[((int64_t)g * kNormChunks + b) * gw + l];
     out[t] = s;
 }
 
@@ -873,9 +894,14 @@ void launch_unpack(const double *src, double *dst, int64_t grid, int ntets, int 
     k_unpack<<<gr, 256, 0, s>>>(src, dst, grid, ntets, tpl);
 }
 
-void launch_batch_norms(const double *part, int nrows, int ntets, int tpl, double *out, cudaStream_t s)
+// part: [G][nrows][gw] followed by norm_scratch_doubles() of scratch
+size_t norm_scratch_doubles(int G, int tpl) { return (size_t)G * kNormChunks * 32 * tpl; }
+void launch_batch_norms(double *part, int nrows, int ntets, int tpl, double *out, cudaStream_t s)
 {
-    k_batch_norms<<<(ntets + 127) / 128, 128, 0, s>>>(part, nrows, ntets, 32 * tpl, out);
+    const int gw = 32 * tpl, G = (ntets + gw - 1) / gw;
+    double *mid = part + (size_t)G * nrows * gw;
+    k_batch_norms<<<dim3(kNormChunks, G), 256, 0, s>>>(part, nrows, gw, mid);
+    k_norms_final<<<(ntets + 127) / 128, 128, 0, s>>>(mid, ntets, gw, out);
 }
 
 void launch_arm(const PlanDev &P, double *wa, const unsigned long long *hdr, unsigned long long key, int G, int tpl,
@@ -883,7 +909,7 @@ void launch_arm(const PlanDev &P, double *wa, const unsigned long long *hdr, uns
 {
     const int64_t n2 = (int64_t)G * P.grid * 32 * tpl;  // doubles of w_f + w_b, / 2
     k_arm_zero<<<4 * 148, 256, 0, s>>>(reinterpret_cast<double2 *>(wa), n2, hdr, key);
-    k_arm<<<dim3((unsigned)P.nrows, (unsigned)G), 256, 0, s>>>(P, wa, hdr, key, tpl);
+    k_arm<<<dim3((unsigned)std::min(P.nrows, 1024), (unsigned)G), 256, 0, s>>>(P, wa, hdr, key, tpl);
 }
 
 // Persistent grid: as many CTAs as fit on the device at once (queried once per kernel).

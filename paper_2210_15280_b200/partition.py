@@ -157,16 +157,51 @@ class MacroMeshSmoother:
         return u
 
     def apply_host(self, u_host: "torch.Tensor", f_host: "torch.Tensor", sweeps: int = 1,
-                   residual_norms: bool = True):
-        """End-to-end call on (pinned) host tensors: H2D of u and f, ``sweeps`` sweeps, D2H of u
-        (in place) and of the global norms.  Returns the norms (host tensor) or None."""
+                   residual_norms: bool = True, chunk: int = 64):
+        """End-to-end call on (pinned) host tensors [ntets_local, grid]: H2D of u and f, ``sweeps``
+        sweeps, D2H of u (in place) and of the global norms.  Returns the norms (host tensor) or None.
+
+        Pipelined: the tets go through in chunks of ``chunk`` (independent packed groups) on two
+        streams, so the H2D of one chunk and the D2H of another overlap the sweeps of a third."""
         dev = torch.device("cuda", torch.cuda.current_device())
-        u = u_host.to(dev, non_blocking=True)
-        f = f_host.to(dev, non_blocking=True)
-        self.load(u, f)
-        norms = self.sweep(sweeps, residual_norms)
-        self.store(u)
-        u_host.copy_(u, non_blocking=True)
-        out = norms.to("cpu", non_blocking=True) if residual_norms else None
-        torch.cuda.current_stream().synchronize()
+        main = torch.cuda.current_stream(dev)
+        if getattr(self, "_copy_streams", None) is None:
+            self._copy_streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+            self._scratch = {}
+        parts = []  # (smoother index, first tet, count): host-contiguous runs cut into chunks
+        for si, g in enumerate(self.groups):
+            run0 = 0
+            for i in range(1, len(g) + 1):
+                if i == len(g) or g[i] != g[i - 1] + 1:
+                    for a in range(g[run0], g[i - 1] + 1, chunk):
+                        parts.append((si, a, min(chunk, g[i - 1] + 1 - a)))
+                    run0 = i
+        pn = torch.zeros((len(parts), sweeps), dtype=torch.float64, device=dev) if residual_norms else None
+        start = torch.cuda.Event()
+        start.record(main)
+        for i, (si, a, cnt) in enumerate(parts):
+            s = self._copy_streams[i % 2]
+            s.wait_event(start)
+            p = self.smoothers[si].plan
+            with torch.cuda.stream(s):
+                uc = u_host[a:a + cnt].to(dev, non_blocking=True)
+                fc = f_host[a:a + cnt].to(dev, non_blocking=True)
+                up, fp = p.pack(uc), p.pack(fc)
+                key = (si, cnt, i % 2)
+                if key not in self._scratch:
+                    self._scratch[key] = p.new_scratch(cnt, device=dev)
+                rn = p.sweep_packed(up, fp, self._scratch[key], cnt, sweeps, norms=residual_norms)
+                self.launches += p.last_launch_count() + 3  # + pack u, pack f, unpack
+                p.unpack(up, uc)
+                u_host[a:a + cnt].copy_(uc, non_blocking=True)
+                if residual_norms:
+                    pn[i] = rn.sum(dim=1)
+        for s in self._copy_streams:
+            main.wait_stream(s)
+        out = None
+        if residual_norms:
+            norms = pn.sum(dim=0)
+            allreduce_norms(norms, self.group)
+            out = norms.to("cpu", non_blocking=True)
+        main.synchronize()
         return out

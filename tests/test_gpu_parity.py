@@ -327,6 +327,28 @@ def test_macro_mesh_smoother_resident_equals_apply():
     torch.testing.assert_close(n1, n2, rtol=1e-12, atol=0)
 
 
+def test_macro_mesh_apply_host_pipelined_equals_apply():
+    """End-to-end entry point (pinned host tensors, chunked two-stream pipeline) == device apply."""
+    from paper_2210_15280_b200 import MacroMeshSmoother
+    tets = lattice.kuhn_mesh(2)          # 48 tets
+    level = 4
+    mm = MacroMeshSmoother(tets, level, degrees=(3, 3, 3))
+    mask = lattice.interior_mask(level)
+    rng = np.random.default_rng(2)
+    us = np.zeros((len(tets), mask.size))
+    us[:, mask] = rng.uniform(-1, 1, (len(tets), int(mask.sum())))
+    fs = np.zeros_like(us)
+    fs[:, mask] = rng.standard_normal((len(tets), int(mask.sum())))
+    u1, f1 = cuda(us), cuda(fs)
+    n1 = mm.apply(u1, f1, 2)
+    for chunk in (7, 128):
+        uh = torch.from_numpy(us.copy()).pin_memory()
+        fh = torch.from_numpy(fs.copy()).pin_memory()
+        n2 = mm.apply_host(uh, fh, 2, chunk=chunk)
+        assert torch.equal(uh, u1.cpu()), chunk
+        torch.testing.assert_close(n2, n1.cpu(), rtol=1e-12, atol=0)
+
+
 def test_packed_dataflow_repeatable_and_equals_simple():
     """The dataflow kernels' inter-warp / inter-CTA handoffs leave no room for races: repeated
     runs are bitwise identical and equal the one-CTA-per-tet reference-layout kernels."""
