@@ -143,13 +143,15 @@ __device__ __forceinline__ Vt<T> ldsv(const double *p)
     return ldv<T>(p);
 }
 
-// Per-warp ring of D stages.  Stage = NS streams of one point (GW doubles each) + 8 coefficient
-// doubles (TAB).  Lane 0 issues the bulk copies of point p; every lane waits on the stage's
-// mbarrier and reads its own T values.  Issue and consume run in the same order through one
-// sequence counter per warp (stage = seq % D, parity = (seq / D) & 1).
-template <int NS, int GW, int D>
+// Per-warp ring of D stages, each holding one chunk of P consecutive points of a row: NS streams
+// ([NS][P][GW] doubles) + P coefficient records of 8 doubles (TAB).  Lane 0 issues one bulk copy
+// per stream per chunk (a row's points are contiguous), so the copy-issue cost is shared by P
+// points; every lane waits on the stage's mbarrier at the chunk's first point and reads its own T
+// values.  Issue and consume run in the same order through one sequence counter per warp
+// (stage = seq % D, parity = (seq / D) & 1).
+template <int NS, int GW, int D, int P>
 struct Ring {
-    static constexpr int SD = NS * GW + 8;  // doubles per stage
+    static constexpr int SD = NS * P * GW + 8 * P;  // doubles per stage
     double *buf;
     uint64_t *mb;
     uint32_t iss, con;
@@ -293,18 +295,19 @@ __device__ __forceinline__ void fwd_band_load(double &dst, const PlanDev &P, con
 }
 
 // Shared memory of the forward / backward kernels: per warp, D mbarriers + D ring stages.
-template <int NS, int T, int D>
-constexpr size_t ring_smem() { return (size_t)kWarps * D * (8 + (NS * 32 * T + 8) * 8); }
+constexpr int kChunk = 2;   // points per ring stage (per bulk copy)
 template <int T>
-constexpr int kStages = T == 4 ? 2 : 4;  // ring depth (points in flight per warp)
+constexpr int kStages = 2;  // ring depth in chunks (kStages * kChunk points in flight per warp)
+template <int NS, int T, int D>
+constexpr size_t ring_smem() { return (size_t)kWarps * D * (8 + (NS * kChunk * 32 * T + 8 * kChunk) * 8); }
 constexpr int kFwdNS = 8;    // forward ring streams: ue us un ubn ubc uts utc f
 constexpr int kBwdNS = 2;    // backward ring streams: w_f(p), u(p)
 
 template <int K, bool EXACT, bool CONST_ROW, int T, bool TAB>
 __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_batch_fwd(PlanDev P, BatchArgs A)
 {
-    constexpr int GW = 32 * T, D = kStages<T>, NS = kFwdNS;
-    using RingT = Ring<NS, GW, D>;
+    constexpr int GW = 32 * T, D = kStages<T>, NS = kFwdNS, PC = kChunk;
+    using RingT = Ring<NS, GW, D, PC>;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_tab[kWarps][7 * K];
     __shared__ double s_L[kWarps][8];
@@ -349,27 +352,29 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
         R.boff = P.variant == 1 ? P.bandoff[R.rid] : 0;
         const int m = R.m;
         const double *cf = P.coefF + 8 * ((int64_t)(R.oc / GW));  // TAB: coefficients of (0, y, z)
-        // ring producer: point p's u/f segments (+ coefficients) into the next stage
-        auto issue = [&](int p) {
+        // ring producer: chunk c (points c*P+1 ..) of the u/f rows (+ coefficients) into the next stage
+        const int nch = (m + PC - 1) / PC;
+        auto issue = [&](int c) {
             if (lane == 0) {
-                const uint32_t X = (uint32_t)p * GW, B = GW * 8;
+                const int x0 = c * PC + 1, np = min(PC, m - c * PC);
+                const uint32_t X = (uint32_t)x0 * GW, B = (uint32_t)np * GW * 8;
                 double *st = ring.stage(ring.iss);
                 uint64_t *mb = &ring.mb[ring.iss % D];
-                mbar_expect_tx(mb, NS * B + (TAB ? 64u : 0u));
-                bulk_g2s(st + 0 * GW, ug + R.oc + X + GW, B, mb);   // ue
-                bulk_g2s(st + 1 * GW, ug + R.os + X + GW, B, mb);   // us
-                bulk_g2s(st + 2 * GW, ug + R.on + X, B, mb);        // un
-                bulk_g2s(st + 3 * GW, ug + R.obn + X, B, mb);       // ubn
-                bulk_g2s(st + 4 * GW, ug + R.obc + X + GW, B, mb);  // ubc
-                bulk_g2s(st + 5 * GW, ug + R.ots + X + GW, B, mb);  // uts
-                bulk_g2s(st + 6 * GW, ug + R.otc + X, B, mb);       // utc
-                bulk_g2s(st + 7 * GW, fg + R.oc + X, B, mb);        // f
-                if (TAB) bulk_g2s(st + NS * GW, cf + 8 * p, 64, mb);
+                mbar_expect_tx(mb, NS * B + (TAB ? 64u * np : 0u));
+                bulk_g2s(st + 0 * PC * GW, ug + R.oc + X + GW, B, mb);   // ue
+                bulk_g2s(st + 1 * PC * GW, ug + R.os + X + GW, B, mb);   // us
+                bulk_g2s(st + 2 * PC * GW, ug + R.on + X, B, mb);        // un
+                bulk_g2s(st + 3 * PC * GW, ug + R.obn + X, B, mb);       // ubn
+                bulk_g2s(st + 4 * PC * GW, ug + R.obc + X + GW, B, mb);  // ubc
+                bulk_g2s(st + 5 * PC * GW, ug + R.ots + X + GW, B, mb);  // uts
+                bulk_g2s(st + 6 * PC * GW, ug + R.otc + X, B, mb);       // utc
+                bulk_g2s(st + 7 * PC * GW, fg + R.oc + X, B, mb);        // f
+                if (TAB) bulk_g2s(st + NS * PC * GW, cf + 8 * x0, 64u * np, mb);
             }
             ++ring.iss;
         };
         __syncwarp();  // every lane is done with the stages about to be refilled
-        for (int p = 1; p <= min(D, m); ++p) issue(p);
+        for (int c = 0; c < min(D, nch); ++c) issue(c);
         if constexpr (!TAB) smem_load_table<7, K>(tab, P.seedF + (int64_t)R.rid * 7 * K, lane);
         // sliding windows (values of point x-1 / x that point x+1 reuses)
         Vt<T> u_wm = ldv<T>(u + R.oc), u_c = ldv<T>(u + R.oc + GW), us0 = ldv<T>(u + R.os + GW);
@@ -397,18 +402,21 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
             double a[15];
 #pragma unroll
             for (int i = 0; i < 15; ++i) a[i] = CONST_ROW ? A.arow[i] : P.arows[15 * (int64_t)(R.oc / GW + x) + i];
-            // this point's u/f (and coefficients) from the ring
-            const double *st = ring.stage(ring.con);
-            mbar_wait(&ring.mb[ring.con % D], (ring.con / D) & 1);
-            ++ring.con;
-            const double *sl = st + lane * T;
-            const Vt<T> ue = ldsv<T>(sl + 0 * GW), us = ldsv<T>(sl + 1 * GW), un = ldsv<T>(sl + 2 * GW);
-            const Vt<T> ubn = ldsv<T>(sl + 3 * GW), ubc = ldsv<T>(sl + 4 * GW), uts = ldsv<T>(sl + 5 * GW);
-            const Vt<T> utc = ldsv<T>(sl + 6 * GW), fv = ldsv<T>(sl + 7 * GW);
+            // this point's u/f (and coefficients) from the ring (wait once per chunk)
+            const int slot = (x - 1) % PC;
+            if (slot == 0) {
+                mbar_wait(&ring.mb[ring.con % D], (ring.con / D) & 1);
+                ++ring.con;
+            }
+            const double *st = ring.stage(ring.con - 1);
+            const double *sl = st + slot * GW + lane * T;
+            const Vt<T> ue = ldsv<T>(sl + 0 * PC * GW), us = ldsv<T>(sl + 1 * PC * GW), un = ldsv<T>(sl + 2 * PC * GW);
+            const Vt<T> ubn = ldsv<T>(sl + 3 * PC * GW), ubc = ldsv<T>(sl + 4 * PC * GW), uts = ldsv<T>(sl + 5 * PC * GW);
+            const Vt<T> utc = ldsv<T>(sl + 6 * PC * GW), fv = ldsv<T>(sl + 7 * PC * GW);
             double L[7];
             if constexpr (TAB) {
 #pragma unroll
-                for (int i = 0; i < 7; ++i) L[i] = st[NS * GW + i];
+                for (int i = 0; i < 7; ++i) L[i] = st[NS * PC * GW + 8 * slot + i];
             } else {
                 if (lane < 7) sL[lane] = (P.variant == 1 && in_band_b(x, y, z, m)) ? cband : tab[lane * K];
                 __syncwarp();
@@ -466,8 +474,11 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
             stv<T>(wa + R.oc + X, v);
             stv<T>(wb + R.oc + X, sent_v<T>());  // re-arm w_b for the backward pass
             if constexpr (!TAB) smem_march<7, K>(tab, lane);
-            __syncwarp();  // every lane has read this stage: it may be refilled
-            if (x + D <= m) issue(x + D);
+            if (slot == PC - 1 || x == m) {  // chunk consumed by every lane: refill its stage
+                __syncwarp();
+                const int c = (x - 1) / PC;
+                if (c + D < nch) issue(c + D);
+            }
             u_wm = u_c;
             u_c = ue;
             us0 = us;
@@ -549,8 +560,8 @@ __device__ __forceinline__ int bwd_band_load(double &dst, const BwdRow &R, const
 template <int K, bool EXACT, int T, bool TAB>
 __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_batch_bwd(PlanDev P, BatchArgs A)
 {
-    constexpr int GW = 32 * T, D = kStages<T>, NS = kBwdNS;
-    using RingT = Ring<NS, GW, D>;
+    constexpr int GW = 32 * T, D = kStages<T>, NS = kBwdNS, PC = kChunk;
+    using RingT = Ring<NS, GW, D, PC>;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_tab[kWarps][8 * K];
     __shared__ double s_L[kWarps][8];
@@ -590,21 +601,24 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
         R.otc = (uint32_t)row_offset(n, z + 1, y) * GW;
         const int m = R.m;
         const double *cb = P.coefB + 8 * ((int64_t)(R.oc / GW));  // TAB: coefficients of (0, y, z)
-        // ring producer: point x's own w_f and u (+ coefficients); points in descending x
-        auto issue = [&](int x) {
+        // ring producer: chunk c = points x_hi = m - c*P down to x_hi - P + 1 of the own w_f and u
+        // rows (+ coefficients); stage slot i holds x = x_hi - P + 1 + i (ascending, clipped at 1)
+        const int nch = (m + PC - 1) / PC;
+        auto issue = [&](int c) {
             if (lane == 0) {
-                const uint32_t X = (uint32_t)x * GW, B = GW * 8;
+                const int xh = m - c * PC, xl = max(1, xh - PC + 1), np = xh - xl + 1, s0 = xl - (xh - PC + 1);
+                const uint32_t X = (uint32_t)xl * GW, B = (uint32_t)np * GW * 8;
                 double *st = ring.stage(ring.iss);
                 uint64_t *mb = &ring.mb[ring.iss % D];
-                mbar_expect_tx(mb, NS * B + (TAB ? 64u : 0u));
-                bulk_g2s(st + 0 * GW, wag + R.oc + X, B, mb);  // w_f(p): final since the forward pass
-                bulk_g2s(st + 1 * GW, ug + R.oc + X, B, mb);   // u(p)
-                if (TAB) bulk_g2s(st + NS * GW, cb + 8 * x, 64, mb);
+                mbar_expect_tx(mb, NS * B + (TAB ? 64u * np : 0u));
+                bulk_g2s(st + 0 * PC * GW + s0 * GW, wag + R.oc + X, B, mb);  // w_f(p): final since the fwd pass
+                bulk_g2s(st + 1 * PC * GW + s0 * GW, ug + R.oc + X, B, mb);   // u(p)
+                if (TAB) bulk_g2s(st + NS * PC * GW + 8 * s0, cb + 8 * xl, 64u * np, mb);
             }
             ++ring.iss;
         };
         __syncwarp();  // every lane is done with the stages about to be refilled
-        for (int k = 1; k <= min(D, m); ++k) issue(m - k + 1);
+        for (int c = 0; c < min(D, nch); ++c) issue(c);
         if (!TAB && lane < 8) {  // the row of q_m (lane m) or the own row (lane 7)
             const int qy = lane < 7 ? y - kDY[lane] : y, qz = lane < 7 ? z - kDZ[lane] : z;
             const bool valid = qy >= 1 && qz >= 1 && qy + qz <= n - 2;
@@ -632,14 +646,17 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
             const Vt<T> wn_n = ldcgv<T>(wb + R.on + XN - GW), wts_n = ldcgv<T>(wb + R.ots + XN),
                         wtc_n = ldcgv<T>(wb + R.otc + XN - GW);
             if constexpr (!TAB) nsrc = bwd_band_load(nband, R, P, n, z, xn, lane);
-            const double *st = ring.stage(ring.con);
-            mbar_wait(&ring.mb[ring.con % D], (ring.con / D) & 1);
-            ++ring.con;
-            const Vt<T> wf = ldsv<T>(st + lane * T), uo = ldsv<T>(st + GW + lane * T);
+            const int kk = (k - 1) % PC, slot = PC - 1 - kk;
+            if (kk == 0) {
+                mbar_wait(&ring.mb[ring.con % D], (ring.con / D) & 1);
+                ++ring.con;
+            }
+            const double *st = ring.stage(ring.con - 1);
+            const Vt<T> wf = ldsv<T>(st + slot * GW + lane * T), uo = ldsv<T>(st + (PC + slot) * GW + lane * T);
             double L[8];
             if constexpr (TAB) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) L[i] = st[NS * GW + i];
+                for (int i = 0; i < 8; ++i) L[i] = st[NS * PC * GW + 8 * slot + i];
             } else {
                 if (lane < 8) sL[lane] = csrc == 0 ? 0.0 : (csrc == 1 ? cband : tab[lane * K]);
                 __syncwarp();
@@ -682,8 +699,11 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
             stv<T>(u + R.oc + X, un);
             stv<T>(wa + R.oc + X, sent_v<T>());  // re-arm w_f for the next forward pass
             if constexpr (!TAB) smem_march<8, K>(tab, lane);
-            __syncwarp();  // every lane has read this stage: it may be refilled
-            if (k + D <= m) issue(m - (k + D) + 1);
+            if (kk == PC - 1 || k == m) {  // chunk consumed by every lane: refill its stage
+                __syncwarp();
+                const int c = (k - 1) / PC;
+                if (c + D < nch) issue(c + D);
+            }
             wn_hi = wn;
             wts_hi = wts;
             wtc_hi = wtc;
