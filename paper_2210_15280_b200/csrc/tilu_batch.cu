@@ -254,6 +254,15 @@ __device__ __forceinline__ void smem_march(double *tab, int lane)
 // forward: residual + L solve
 // ----------------------------------------------------------------------------------------------
 template <int T>
+struct WNf {  // forward: w_f of the neighbours (x+1, y-1, z), (x, y+1, z-1), (x+1, y, z-1)
+    Vt<T> s, bn, bc;
+};
+template <int T>
+struct WNb {  // backward: w_b of the neighbours (x-1, y+1, z), (x, y-1, z+1), (x-1, y, z+1)
+    Vt<T> n, ts, tc;
+};
+
+template <int T>
 struct FwdSlot {
     Vt<T> ue, us, un, ubn, ubc, uts, utc, f, ws, wbn, wbc;
 };
@@ -389,15 +398,21 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
         // neighbours' w (produced concurrently): direct L2 loads one point ahead (generic 8 / 16-byte
         // loads: single-copy atomic per double, which the sentinel protocol relies on; prefetching
         // further ahead mostly finds sentinels -- the rows run a few points behind their producers)
-        Vt<T> ws = ldcgv<T>(wa + R.os + 2 * GW), wbn = ldcgv<T>(wa + R.obn + GW), wbc = ldcgv<T>(wa + R.obc + 2 * GW);
+        // Two register sets for the prefetched neighbours, used in ping-pong (loop unrolled by two):
+        // copying a value whose load was issued in the same iteration would wait for it.
+        WNf<T> wA, wB;
+        wA.s = ldcgv<T>(wa + R.os + 2 * GW);
+        wA.bn = ldcgv<T>(wa + R.obn + GW);
+        wA.bc = ldcgv<T>(wa + R.obc + 2 * GW);
         double cband = 0.0, nband = 0.0;
         if constexpr (!TAB) fwd_band_load(cband, P, R, z, 1, lane);
-        for (int x = 1; x <= m; ++x) {
+        auto point = [&](const int x, WNf<T> &cw, WNf<T> &nw) {
             const uint32_t X = (uint32_t)x * GW;
             const int pn = min(x + 1, m);  // (at the row end: re-read point m, unused)
             const uint32_t XN = (uint32_t)pn * GW;
-            const Vt<T> ws_n = ldcgv<T>(wa + R.os + XN + GW), wbn_n = ldcgv<T>(wa + R.obn + XN),
-                        wbc_n = ldcgv<T>(wa + R.obc + XN + GW);
+            nw.s = ldcgv<T>(wa + R.os + XN + GW);
+            nw.bn = ldcgv<T>(wa + R.obn + XN);
+            nw.bc = ldcgv<T>(wa + R.obc + XN + GW);
             if constexpr (!TAB) fwd_band_load(nband, P, R, z, pn, lane);
             double a[15];
 #pragma unroll
@@ -424,12 +439,13 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
                 for (int i = 0; i < 7; ++i) L[i] = sL[i];
             }
             TILU_STAT(0, 1);
-            if (__any_sync(0xffffffffu, any_sent(ws) | any_sent(wbn) | any_sent(wbc))) {
+            if (__any_sync(0xffffffffu, any_sent(cw.s) | any_sent(cw.bn) | any_sent(cw.bc))) {
                 TILU_STAT(1, 1);
-                ready<T>(ws, wa + R.os + X + GW);
-                ready<T>(wbn, wa + R.obn + X);
-                ready<T>(wbc, wa + R.obc + X + GW);
+                ready<T>(cw.s, wa + R.os + X + GW);
+                ready<T>(cw.bn, wa + R.obn + X);
+                ready<T>(cw.bc, wa + R.obc + X + GW);
             }
+            const Vt<T> &ws = cw.s, &wbn = cw.bn, &wbc = cw.bc;
             Vt<T> v;
 #pragma unroll
             for (int t = 0; t < T; ++t) {
@@ -490,12 +506,15 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
             ws0 = ws;
             wbn_m = wbn;
             wbc0 = wbc;
-            ws = ws_n;
-            wbn = wbn_n;
-            wbc = wbc_n;
             wprev = v;
             cband = nband;
+        };
+        int x = 1;
+        for (; x + 1 <= m; x += 2) {
+            point(x, wA, wB);
+            point(x + 1, wB, wA);
         }
+        if (x <= m) point(x, wA, wB);
         if (A.part) {
 #pragma unroll
             for (int t = 0; t < T; ++t) A.part[((int64_t)g * P.nrows + ri) * GW + lane * T + t] = ss.a[t];
@@ -634,17 +653,21 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
 #pragma unroll
         for (int t = 0; t < T; ++t) wprev.a[t] = 0.0;
         // neighbours' w_b (produced concurrently): direct L2 loads, one point ahead
-        Vt<T> wn = ldcgv<T>(wb + R.on + M - GW), wts = ldcgv<T>(wb + R.ots + M), wtc = ldcgv<T>(wb + R.otc + M - GW);
+        WNb<T> wA, wB;  // ping-pong prefetch sets (see the forward kernel)
+        wA.n = ldcgv<T>(wb + R.on + M - GW);
+        wA.ts = ldcgv<T>(wb + R.ots + M);
+        wA.tc = ldcgv<T>(wb + R.otc + M - GW);
         double cband = 0.0, nband = 0.0;
         int csrc = 2, nsrc = 2;
         if constexpr (!TAB) csrc = bwd_band_load(cband, R, P, n, z, m, lane);
-        for (int k = 1; k <= m; ++k) {
+        auto point = [&](const int k, WNb<T> &cw, WNb<T> &nw) {
             const int x = m - k + 1;
             const uint32_t X = (uint32_t)x * GW;
             const int xn = max(x - 1, 1);  // (at the row end: re-read x = 1, unused)
             const uint32_t XN = (uint32_t)xn * GW;
-            const Vt<T> wn_n = ldcgv<T>(wb + R.on + XN - GW), wts_n = ldcgv<T>(wb + R.ots + XN),
-                        wtc_n = ldcgv<T>(wb + R.otc + XN - GW);
+            nw.n = ldcgv<T>(wb + R.on + XN - GW);
+            nw.ts = ldcgv<T>(wb + R.ots + XN);
+            nw.tc = ldcgv<T>(wb + R.otc + XN - GW);
             if constexpr (!TAB) nsrc = bwd_band_load(nband, R, P, n, z, xn, lane);
             const int kk = (k - 1) % PC, slot = PC - 1 - kk;
             if (kk == 0) {
@@ -664,12 +687,13 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
                 for (int i = 0; i < 8; ++i) L[i] = sL[i];
             }
             TILU_STAT(0, 1);
-            if (__any_sync(0xffffffffu, any_sent(wn) | any_sent(wts) | any_sent(wtc))) {
+            if (__any_sync(0xffffffffu, any_sent(cw.n) | any_sent(cw.ts) | any_sent(cw.tc))) {
                 TILU_STAT(1, 1);
-                ready<T>(wn, wb + R.on + X - GW);
-                ready<T>(wts, wb + R.ots + X);
-                ready<T>(wtc, wb + R.otc + X - GW);
+                ready<T>(cw.n, wb + R.on + X - GW);
+                ready<T>(cw.ts, wb + R.ots + X);
+                ready<T>(cw.tc, wb + R.otc + X - GW);
             }
+            const Vt<T> &wn = cw.n, &wts = cw.ts, &wtc = cw.tc;
             const double inv_d = L[7];
             Vt<T> v, un;
 #pragma unroll
@@ -707,13 +731,16 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
             wn_hi = wn;
             wts_hi = wts;
             wtc_hi = wtc;
-            wn = wn_n;
-            wts = wts_n;
-            wtc = wtc_n;
             wprev = v;
             cband = nband;
             csrc = nsrc;
+        };
+        int k = 1;
+        for (; k + 1 <= m; k += 2) {
+            point(k, wA, wB);
+            point(k + 1, wB, wA);
         }
+        if (k <= m) point(k, wA, wB);
     }
     // the last warp to finish marks the scratch ready (w_f re-armed everywhere) for the next call
     if (lane == 0) {
