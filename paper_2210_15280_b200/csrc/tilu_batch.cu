@@ -125,6 +125,36 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(b))
                  : "memory");
 }
+// Bulk copy with an L2 eviction policy (streams read once, e.g. f).
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *b, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// Store of the sentinel (re-arm): not read again until the next pass -- evict first.
+template <int T>
+__device__ __forceinline__ void st_sent(double *p, uint64_t pol)
+{
+    const double sv = __longlong_as_double(kSent);
+    if constexpr (T == 1) {
+        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(sv), "l"(pol) : "memory");
+    } else {
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i)
+            asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p + 2 * i), "d"(sv), "d"(sv), "l"(pol)
+                         : "memory");
+    }
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
 {
     asm volatile(
@@ -328,6 +358,7 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
     ring.mb = reinterpret_cast<uint64_t *>(smem) + warp * D;
     ring.buf = reinterpret_cast<double *>(smem + (size_t)kWarps * D * 8) + (size_t)warp * D * RingT::SD;
     ring.iss = ring.con = 0;
+    const uint64_t pol_ef = policy_evict_first();
     if (lane == 0) {
         for (int i = 0; i < D; ++i) mbar_init(&ring.mb[i], 1);
         fence_mbar_init();
@@ -377,7 +408,7 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
                 bulk_g2s(st + 4 * PC * GW, ug + R.obc + X + GW, B, mb);  // ubc
                 bulk_g2s(st + 5 * PC * GW, ug + R.ots + X + GW, B, mb);  // uts
                 bulk_g2s(st + 6 * PC * GW, ug + R.otc + X, B, mb);       // utc
-                bulk_g2s(st + 7 * PC * GW, fg + R.oc + X, B, mb);        // f
+                bulk_g2s_hint(st + 7 * PC * GW, fg + R.oc + X, B, mb, pol_ef);  // f (read once)
                 if (TAB) bulk_g2s(st + NS * PC * GW, cf + 8 * x0, 64u * np, mb);
             }
             ++ring.iss;
@@ -488,7 +519,7 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
                 v.a[t] = vv;
             }
             stv<T>(wa + R.oc + X, v);
-            stv<T>(wb + R.oc + X, sent_v<T>());  // re-arm w_b for the backward pass
+            st_sent<T>(wb + R.oc + X, pol_ef);  // re-arm w_b for the backward pass
             if constexpr (!TAB) smem_march<7, K>(tab, lane);
             if (slot == PC - 1 || x == m) {  // chunk consumed by every lane: refill its stage
                 __syncwarp();
@@ -592,6 +623,7 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
     ring.mb = reinterpret_cast<uint64_t *>(smem) + warp * D;
     ring.buf = reinterpret_cast<double *>(smem + (size_t)kWarps * D * 8) + (size_t)warp * D * RingT::SD;
     ring.iss = ring.con = 0;
+    const uint64_t pol_ef = policy_evict_first();
     if (lane == 0) {
         for (int i = 0; i < D; ++i) mbar_init(&ring.mb[i], 1);
         fence_mbar_init();
@@ -721,7 +753,7 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
             }
             stv<T>(wb + R.oc + X, v);
             stv<T>(u + R.oc + X, un);
-            stv<T>(wa + R.oc + X, sent_v<T>());  // re-arm w_f for the next forward pass
+            st_sent<T>(wa + R.oc + X, pol_ef);  // re-arm w_f for the next forward pass
             if constexpr (!TAB) smem_march<8, K>(tab, lane);
             if (kk == PC - 1 || k == m) {  // chunk consumed by every lane: refill its stage
                 __syncwarp();
