@@ -43,6 +43,8 @@ extern "C" {
 #define TILU_FAST 0x1     /* fused (FMA) substitution + residual: <= 1e-12 rel. vs the reference,
                              not bitwise.  Default: exact reference operation order. */
 #define TILU_SCHED_SIMPLE 0x2 /* force the reference-layout wavefront kernels (no plane layout) */
+#define TILU_SCHED_PLANE 0x4  /* single tets: plane-layout band kernels at every level >= 3 (default: >= 5) */
+#define TILU_SCHED_BATCH 0x8  /* single tets: never the plane kernels (interleaved dataflow kernels instead) */
 
 typedef struct tilu_plan tilu_plan_t;
 

@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("TILU_LIB", os.path.join(_HERE, "lib", "libtilu.so"))
 
 TILU_OK, TILU_EINVAL, TILU_ECUDA, TILU_ENOMEM, TILU_EUNSUPPORTED, TILU_EPIVOT = range(6)
 VARIANT_V1, VARIANT_V2 = 1, 2
-FLAG_FAST, FLAG_SCHED_SIMPLE = 0x1, 0x2
+FLAG_FAST, FLAG_SCHED_SIMPLE, FLAG_SCHED_PLANE, FLAG_SCHED_BATCH = 0x1, 0x2, 0x4, 0x8
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int

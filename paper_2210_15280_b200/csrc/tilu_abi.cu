@@ -40,6 +40,7 @@ void launch_arm(const PlanDev &P, double *wa, const unsigned long long *hdr, uns
 void prof_begin(cudaStream_t s);
 void prof_end(const char *name, cudaStream_t s);
 bool plane_supported(const tilu_plan *plan);
+void plane_free(void *ws);
 int plane_sweep(const tilu_plan *plan, double *u, const double *f, int ntets, int sweeps, double *rnorm2,
                 cudaStream_t s, int *launches);
 }  // namespace tilu
@@ -138,6 +139,13 @@ struct Scratch {
 
 bool valid_plan(const tilu_plan_t *p) { return p != nullptr && p->dev.n > 0; }
 }  // namespace
+
+// Smallest level routed to the plane kernels (TILU_PLANE_MIN_LEVEL overrides, tests use 3).
+static int plane_min_level()
+{
+    static const char *e = std::getenv("TILU_PLANE_MIN_LEVEL");
+    return e ? std::atoi(e) : 5;
+}
 
 bool batch_ok(const tilu_plan_t *p)
 {
@@ -323,6 +331,7 @@ void tilu_plan_destroy(tilu_plan_t *p)
     if (!p) return;
     for (int i = 0; i < p->nallocs; ++i) cudaFree(p->allocs[i]);
     if (p->coef) cudaFree(p->coef);
+    plane_free(p->plane);
     delete p;
 }
 
@@ -564,6 +573,15 @@ static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int nt
     if (sweeps == 0) return TILU_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const PlanDev &P = p->dev;
+    // One macro-tet: the plane-layout band kernels (tilu_plane.cu) parallelise the sweep inside the tet.
+    if (!stored && ntets == 1 && plane_supported(p) && !(p->flags & TILU_SCHED_BATCH) &&
+        ((p->flags & TILU_SCHED_PLANE) || P.level >= plane_min_level())) {
+        int nl = 0;
+        const int rc = plane_sweep(p, u, f, ntets, sweeps, rnorm2, s, &nl);
+        g_launches += nl;
+        if (rc) return fail(rc, "plane sweep failed (%d): %s", rc, cudaGetErrorString(cudaGetLastError()));
+        return check_cuda("plane sweep");
+    }
     // Batched dataflow kernels for several tets, and for one large tet (1 tet in a 32-lane group still
     // beats the one-CTA-per-tet reference-layout kernels by ~10x from level 6 up: tools/single_tet.py).
     if (!stored && batch_ok(p) && (ntets >= 2 || P.level >= 6)) {

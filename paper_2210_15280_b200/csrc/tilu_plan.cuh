@@ -54,6 +54,7 @@ struct tilu_plan {
     int64_t nband;
     int ky1a, kz1a;
     void *coef;  // coefficient tables (2 x [grid][8] doubles), lazily built; freed with the plan
+    void *plane;  // plane-layout workspace of the single-tet path (tilu_plane.cu), lazily built
     // owned device allocations
     void *allocs[16];
     int nallocs;

@@ -53,7 +53,11 @@ class DevicePlan:
     """Owner of one ``tilu_plan_t`` (coefficients, band rows, operator and seed tables on device)."""
 
     def __init__(self, level: int, lcoefs, dcoefs, variant: str = "v1", band_ranks=None, store_rows=None,
-                 arow=None, arows=None, acoefs=None, factors=None, fast: bool = False, simple: bool = False):
+                 arow=None, arows=None, acoefs=None, factors=None, fast: bool = False, simple: bool = False,
+                 schedule: str = "auto"):
+        """schedule: "auto" (single tets: plane kernels from level 5, batches: interleaved kernels),
+        "simple" (reference-layout wavefront kernels), "plane" (plane kernels at every level),
+        "batch" (interleaved dataflow kernels for single tets too)."""
         L = _lib.lib()
         self.level = int(level)
         self.variant = variant
@@ -83,7 +87,12 @@ class DevicePlan:
             d.akx1, d.aky1, d.akz1 = ac.shape[1:]
         if factors is not None:
             d.factors = self._ptr(_f64(factors))
-        d.flags = (_lib.FLAG_FAST if fast else 0) | (_lib.FLAG_SCHED_SIMPLE if simple else 0)
+        if schedule not in ("auto", "simple", "plane", "batch"):
+            raise ValueError(f"unknown schedule {schedule!r}")
+        simple = simple or schedule == "simple"
+        d.flags = ((_lib.FLAG_FAST if fast else 0) | (_lib.FLAG_SCHED_SIMPLE if simple else 0)
+                   | (_lib.FLAG_SCHED_PLANE if schedule == "plane" else 0)
+                   | (_lib.FLAG_SCHED_BATCH if schedule == "batch" else 0))
         self.fast = fast
         handle = ctypes.c_void_p()
         _lib.check(L.tilu_plan_create(ctypes.byref(d), ctypes.byref(handle)))

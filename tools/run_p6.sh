@@ -1,0 +1,5 @@
+LEVEL=8 SWEEPS=1 SCHED=plane TILU_PLANE_TRACE=gpurun_out/p6_trace_L8.txt timeout 300 python tools/plane_bench.py > gpurun_out/p6_bench_L8.log 2>&1
+LEVEL=8 SWEEPS=1 SCHED=plane TILU_PLANE_CTAS_PER_SM=1 TILU_PLANE_TRACE=gpurun_out/p6_trace_L8_c1.txt timeout 300 python tools/plane_bench.py > gpurun_out/p6_bench_L8_c1.log 2>&1
+LEVEL=8 SWEEPS=2 SCHED=plane timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_plane_fwd" -s 2 -c 1 -o gpurun_out/p6_full -f python tools/plane_bench.py > gpurun_out/p6_ncu.log 2>&1
+ncu -i gpurun_out/p6_full.ncu-rep --page raw --csv > gpurun_out/p6_full_raw.csv 2>/dev/null
+ncu -i gpurun_out/p6_full.ncu-rep --page source --csv --print-source sass > gpurun_out/p6_source.csv 2>/dev/null
