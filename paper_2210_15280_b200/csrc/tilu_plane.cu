@@ -42,6 +42,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include <cuda.h>
@@ -56,17 +57,18 @@ void prof_end(const char *name, cudaStream_t s);
 
 namespace pl {
 
-constexpr int PW = 4;    // diagonals (warps) per band
-constexpr int GS = 4;    // unroll factor == global handoff prefetch distance (steps)
-constexpr int TG = 8;    // steps staged by one pair of TMA tensor copies
-constexpr int NG = 2;    // TMA ring depth (groups of TG steps) per warp
-constexpr int HR = 16;   // shared-memory handoff ring depth (steps)
+constexpr int PW = 4;    // diagonals per band (one solver warp + helper warps each)
+constexpr int GS = 4;    // steps per group: helper ring and TMA unit, unroll factor, global prefetch distance
+constexpr int NS = 2;    // helper -> solver ring depth (groups)
+constexpr int NT = 3;    // TMA ring depth (groups)
+constexpr int HR = 8;    // solver -> solver handoff ring depth (steps), power of two
+constexpr int PD = 8;    // global handoff prefetch distance (steps), power of two
 constexpr int WIN = 34;  // doubles per staged line: z0-1 .. z0+32
-// one staged group: forward u box [3 planes s-1..s+1][TG+2 lines][WIN] + f box [TG][WIN];
-// backward w_f box [TG][WIN] + u box [TG][WIN]
-// (tensor copies need 128-byte aligned shared-memory destinations)
-constexpr int FOFF = (3 * (TG + 2) * WIN * 8 + 127) / 128 * 128 / 8;  // doubles: f box offset in a slot
-constexpr int SLOT = (FOFF * 8 + TG * WIN * 8 + 127) / 128 * 128;
+// one staged group: forward u box [3 planes s-1..s+1][GS+4 lines][WIN] + f box [GS][WIN];
+// backward w_f box [GS][WIN] + u box [GS][WIN]  (tensor copies need 128-byte aligned destinations)
+constexpr int FOFF = (3 * (GS + 4) * WIN * 8 + 127) / 128 * 128 / 8;  // doubles: f box offset in a slot
+constexpr int UOFF = (GS * WIN * 8 + 127) / 128 * 128 / 8;            // doubles: backward u box offset
+constexpr int TSLOT = (FOFF * 8 + GS * WIN * 8 + 127) / 128 * 128;
 constexpr int TR = 4 + 3 * PW;  // trace record: start ns, end ns, sm, cta, per warp: cycles total / slow path / waits
 constexpr long long kSentP = 0x7FF4DEADBEEF0002ll;  // signalling NaN: "not produced yet"
 
@@ -85,7 +87,7 @@ __host__ inline Geo make_geo(int n)
 __host__ inline int64_t plane_elems(const Geo &g) { return (int64_t)(g.n + 1) * g.TP * g.ZP; }
 
 // TMA tensor maps over the planes ([s][tau][z], z fastest; out-of-range boxes are zero-filled):
-// u3 = u, box (WIN, TG+2, 3); f1 = f, box (WIN, TG, 1); w1 = w_f, box (WIN, TG, 1); u1 = u, box (WIN, TG, 1).
+// u3 = u, box (WIN, GS+4, 3); f1 = f, box (WIN, GS, 1); w1 = w_f, box (WIN, GS, 1); u1 = u, box (WIN, GS, 1).
 struct Maps {
     CUtensorMap u3, f1, w1, u1;
 };
@@ -99,8 +101,10 @@ struct Args {
     int ntasks;
     int *ticket;           // zeroed per pass
     double *part;          // [ntasks][PW * 32] residual partial sums (forward) or nullptr
+    long long *steplog;    // TILU_PLANE_STEPLOG: [PW][2048] clock64 at every step of task 0 (or nullptr)
     long long *trace;      // TILU_PLANE_TRACE: [ntasks][4] = start ns, end ns, sm id, CTA (or nullptr)
     Geo g;
+    int dbg;               // TILU_PLANE_DBG bits (timing experiments only, results invalid): 1 = no global handoff loads
     double arow[15];       // constant stencil (kernel-parameter bank)
 };
 
@@ -144,17 +148,21 @@ __device__ __forceinline__ void tma3(void *dst, const CUtensorMap *map, int c0, 
 }
 __device__ __forceinline__ double sentv() { return __longlong_as_double(kSentP); }
 __device__ __forceinline__ bool is_sent(double v) { return __double_as_longlong(v) == kSentP; }
-__device__ __forceinline__ double lds_vol(const double *p)
+// Handoff-ring accesses: volatile (re-read every time, never cached in registers) but without a
+// compiler memory clobber, so independent loads and arithmetic still schedule around them.
+__device__ __forceinline__ double lds_vol(const double *p) { return *reinterpret_cast<const volatile double *>(p); }
+__device__ __forceinline__ void sts(double *p, double v) { *reinterpret_cast<volatile double *>(p) = v; }
+__device__ __forceinline__ double ldg_cg(const double *p) { return __ldcg(p); }
+// Speculative prefetch of a handoff value: a weak (L1-cacheable, pipelined) load.  Safe because a
+// handoff position only ever changes once per pass (sentinel -> final value) and L1 starts every
+// kernel empty: a stale copy can only be the sentinel, which sends the consumer to the strong
+// polling path (ldg_cg).
+__device__ __forceinline__ double ldg_pf(const double *p)
 {
     double v;
-    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(su32(p)) : "memory");
+    asm("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));  // weak, not volatile: may be scheduled freely
     return v;
 }
-__device__ __forceinline__ void sts(double *p, double v)
-{
-    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(su32(p)), "d"(v) : "memory");
-}
-__device__ __forceinline__ double ldg_cg(const double *p) { return __ldcg(p); }
 __device__ __forceinline__ long long gtimer()
 {
     long long t;
@@ -205,11 +213,30 @@ __device__ __forceinline__ int band_off(int x, int y, int z) { return (z == 1 ||
 
 // Shared memory of one CTA.
 struct Smem {
-    alignas(128) unsigned char tbuf[PW][NG][SLOT];  // TMA ring (groups of TG steps)
-    double hring[PW][HR][32];                       // handoff ring k: written by warp k-1, read by warp k
-    uint64_t mbar[PW][NG];
+    alignas(128) unsigned char tbuf[PW][NT][TSLOT];  // TMA ring (groups of GS steps)
+    double ring[PW][NS][GS][8][32];                 // helpers -> solver: per step 7 L values + residual (fwd)
+                                                    // or 7 source-point L values + 1/D (bwd)
+    double hring[PW][HR][32];                       // solver k-1 -> solver k handoff ring
+    double pre[PW][PD][3][32];                      // prefetched global handoff values (cp.async)
+    uint64_t tfull[PW][NT];                         // TMA group landed
+    uint64_t full[PW][NS];                          // helpers filled a ring group
+    uint64_t empty[PW][NS];                         // solver drained a ring group
     int task;
 };
+
+// Asynchronous 8-byte global -> shared copies (LDGSTS), tracked by commit groups instead of register
+// scoreboards, so a deep prefetch really stays in flight.
+__device__ __forceinline__ void cpa8(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_pd() { asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory"); }
+
+__device__ __forceinline__ void mb_arrive(uint64_t *b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
 
 // Predicated global load (no branch): v = p ? *ptr : other.
 __device__ __forceinline__ double ld_if(bool p, const double *ptr, double other)
@@ -270,64 +297,217 @@ __device__ __forceinline__ double bwd_chain(double inv_d, double wf, const doubl
     return acc;
 }
 
+template <int HELPERS>
 __device__ __forceinline__ void init_smem(Smem &S)
 {
     for (int i = threadIdx.x; i < PW * HR * 32; i += blockDim.x) (&S.hring[0][0][0])[i] = sentv();
-    if (threadIdx.x < PW * NG) mb_init(&S.mbar[0][0] + threadIdx.x, 1);
+    if (threadIdx.x < PW * NT) mb_init(&S.tfull[0][0] + threadIdx.x, 1);
+    if (threadIdx.x < PW * NS) {
+        mb_init(&S.full[0][0] + threadIdx.x, 32 * HELPERS);
+        mb_init(&S.empty[0][0] + threadIdx.x, 32);
+    }
     mb_fence_init();
     __syncthreads();
 }
 
+__device__ __forceinline__ void trace_start(const Args &A, int t)
+{
+    if (A.trace && threadIdx.x == 0) A.trace[TR * (int64_t)t] = gtimer();
+}
+__device__ __forceinline__ void trace_end(const Args &A, int t)
+{
+    if (A.trace && threadIdx.x == 0) {
+        A.trace[TR * (int64_t)t + 1] = gtimer();
+        A.trace[TR * (int64_t)t + 2] = smid();
+        A.trace[TR * (int64_t)t + 3] = blockIdx.x;
+    }
+}
+
+// The solver's handoff with the neighbouring diagonals (both passes).  Producer back-pressure: before
+// a group of GS steps, the GS ring slots it will write must be armed (consumed).
+__device__ __forceinline__ void wait_armed(const double *hout, int t_first, int dir, int lo, int hi)
+{
+    long long spins = 0;
+    for (;;) {
+        bool busy = false;
+#pragma unroll
+        for (int k = 0; k < GS; ++k) {
+            const int tt = t_first + dir * k;
+            if (tt >= lo && tt <= hi) busy |= !is_sent(lds_vol(hout + (tt & (HR - 1)) * 32));
+        }
+        if (!__any_sync(0xffffffffu, busy)) break;
+        if (++spins > (1ll << 28)) __trap();
+    }
+}
+
+// TILU_PLANE_STEPLOG instrumentation (task 0 only): per warp cycle counters
+// (compiled in only with -DTILU_PLANE_PROF)
+#ifdef TILU_PLANE_PROF
+#define PLN_T0() const long long _pt0 = prof ? clock64() : 0
+#define PLN_ADD(i) do { if (prof) pc[i] += clock64() - _pt0; } while (0)
+#else
+#define PLN_T0() (void)0
+#define PLN_ADD(i) (void)0
+#endif
+
 // ------------------------------------------------------------------------------------------------
 // Forward pass: residual r = f - A u, forward L substitution (unit lower), w_f = result.
 //
-// Iteration sg (= "sigma") computes the residual of step sg (staged lines of step sg) and the
-// substitution of step tau = sg - 1, whose residual was computed one iteration earlier: the
-// 15-term residual chain is off the substitution's critical path.  The inputs produced by other
-// warps are taken speculatively (one volatile shared load / one prefetched global load issued at
-// the top of the iteration) and validated once at the end; only a value that was still the
-// sentinel sends the warp through the slow (polling) path.
+// Per diagonal of the band three warps: the solver (role 0) runs only the substitution chain and
+// the handoffs -- a short dependent sequence per step -- while the march helper (role 1: the seven
+// L values of every point, NDDF march and V1 band rows) and the residual helper (role 2: the
+// 15-point residual from TMA-staged planes) run ahead and pass their results through a
+// shared-memory ring of GS-step groups (mbarrier full / empty).
 // ------------------------------------------------------------------------------------------------
 template <int K, bool EXACT, bool CONST_ROW>
-__global__ void __launch_bounds__(PW * 32, 1) k_plane_fwd(const PlanDev P, const Args A, const __grid_constant__ Maps M)
+__global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, const Args A, const __grid_constant__ Maps M)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    init_smem(S);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k = wid % PW, role = wid / PW;
+    init_smem<2>(S);
     const Geo g = A.g;
     const int n = P.n, ZP = g.ZP;
-    uint32_t gcon = 0, giss = 0;  // TMA groups consumed / issued by this warp (all tasks)
+    uint32_t seq = 0, tseq = 0, tiss = 0;  // ring groups used; TMA groups consumed / issued (role 2)
     for (;;) {
         if (threadIdx.x == 0) S.task = atomicAdd(A.ticket, 1);
         __syncthreads();
         const int t = S.task;
         if (t >= A.ntasks) break;
+        trace_start(A, t);
         const int code = A.tasks[t];
         const int b = code >> 16, c = code & 0xffff;
-        if (A.trace && threadIdx.x == 0) A.trace[TR * (int64_t)t] = gtimer();
         const int s0 = 2 + PW * b, z0 = 1 + 32 * c;
-        const int s = s0 + warp, z = z0 + lane, y = s - z;
+        const int s = s0 + k, z = z0 + lane, y = s - z;
         const int xe = n - 1 - s, xe0 = n - 1 - s0;
-        // from tau = z0-3: lane 0's first point (tau = z0+1) reads u(s, tau-1, z0-1), staged at step tau-3
+        // steps from tau = z0-3 (uniform for the band): lane 0's first point is at tau = z0+1
         const int T0 = z0 - 3, T1 = z0 + 32 + xe0;
         const bool wlive = (s <= n - 2) && (z0 <= s - 1);
         const bool live = wlive && (z <= s - 1);
+        const int lo = live ? z + 1 : 1 << 30, hi = live ? z + xe : -(1 << 30);  // steps with a point
+        const int ngroups = (T1 - T0) / GS + 1;
         double r2 = 0.0;
-        double *hin = &S.hring[warp][0][0];
-        double *hout = (warp + 1 < PW) ? &S.hring[warp + 1][0][0] : nullptr;
-        auto hs = [](int tau) { return ((tau + HR) % HR) * 32; };
-        if (!wlive) {
-            // no rows here: pass zeros down the band (the neighbour values are boundary values)
-            for (int tau = T0; tau <= T1; ++tau) {
-                if (warp > 0 && tau <= T1 - 1) (void)take_s(hin + hs(tau + 1) + lane);
-                if (hout && tau >= T0 + 1) put_s(hout + hs(tau) + lane, 0.0);
+#ifdef TILU_PLANE_PROF
+        const bool prof = A.steplog && t == 0;
+        long long pc[6] = {0, 0, 0, 0, 0, 0};
+        const long long pstart = prof ? clock64() : 0;
+#endif
+        if (role == 0) {
+            // ================================ solver ===========================================
+            double *hin = &S.hring[k][0][lane];
+            double *hout = (k + 1 < PW) ? &S.hring[k + 1][0][lane] : nullptr;
+            if (!wlive) {
+                // no rows here: pass zeros down the band (the neighbour values are boundary values)
+                for (int tau = T0; tau <= T1; ++tau) {
+                    if (k > 0 && tau <= T1 - 1) (void)take_s(hin + ((tau + 1) & (HR - 1)) * 32);
+                    if (hout && tau >= T0 + 1) put_s(hout + (tau & (HR - 1)) * 32, 0.0);
+                }
+            } else {
+                // warp 0: P(tau+1) = w_f(s-1, tau+1, z); lane 0: ga = w_f(s, tau-1, z0-1), gb = w_f(s-1, tau, z0-1)
+                const double *pw0 = A.W + pidx(g, s - 1, 1, z);
+                const double *pga = A.W + pidx(g, s, -1, z0 - 1);
+                const double *pgb = A.W + pidx(g, s - 1, 0, z0 - 1);
+                double *pwo = A.W + pidx(g, s, 0, z);
+                double *pbo = A.B + pidx(g, s, 0, z);
+                const bool gp_on = (k == 0), gl_on = (lane == 0);
+                // global handoff inputs of step tau, prefetched PD steps ahead into pre[k][tau & (PD-1)]
+                // (addresses of out-of-range steps stay inside the allocation and read boundary zeros)
+                double *pre = &S.pre[k][0][0][lane];
+                auto prefetch = [&](int tau) {
+                    double *d = pre + (tau & (PD - 1)) * 96;
+                    if (gp_on) cpa8(d, pw0 + tau * ZP);
+                    if (gl_on) {
+                        cpa8(d + 32, pga + tau * ZP);
+                        cpa8(d + 64, pgb + tau * ZP);
+                    }
+                    cpa_commit();
+                };
+                for (int i = 0; i < PD; ++i) prefetch(T0 + i);
+                double w1 = 0, w2 = 0, p1 = 0, p2 = 0, ga_prev = 0, gb_prev = 0;
+                const bool rearm_b = live && (k == 0 || (lane == 0 && z0 > 32));
+                auto grp = [&](const int q) {
+                    const int sl = seq % NS;
+                    const int tq = T0 + GS * q;
+                    {
+                        PLN_T0();
+                        if (hout) wait_armed(hout, tq, 1, T0 + 1, T1);
+                        PLN_ADD(1);
+                    }
+                    {
+                        PLN_T0();
+                        mb_wait(&S.full[k][sl], (seq / NS) & 1);
+                        PLN_ADD(2);
+                    }
+                    const double *rg = &S.ring[k][sl][0][0][lane];
+#pragma unroll
+                    for (int j = 0; j < GS; ++j) {
+                        const int tau = tq + j;
+                        if (tau <= T1) {
+                            const bool p_on = tau <= T1 - 1;
+                            double p0 = 0.0;
+                            cpa_wait_pd();
+                            const double *pv = pre + (tau & (PD - 1)) * 96;
+                            if (p_on) p0 = gp_on ? pv[0] : lds_vol(hin + ((tau + 1) & (HR - 1)) * 32);
+                            double ga_cur = pv[32], gb_cur = pv[64];
+                            double lw1 = __shfl_up_sync(0xffffffffu, w1, 1);
+                            double lw2 = __shfl_up_sync(0xffffffffu, w2, 1);
+                            double lp1 = __shfl_up_sync(0xffffffffu, p1, 1);
+                            double lp2 = __shfl_up_sync(0xffffffffu, p2, 1);
+                            lw1 = gl_on ? ga_cur : lw1;
+                            lw2 = gl_on ? ga_prev : lw2;
+                            lp1 = gl_on ? gb_cur : lp1;
+                            lp2 = gl_on ? gb_prev : lp2;
+                            double L[7];
+#pragma unroll
+                            for (int m = 0; m < 7; ++m) L[m] = rg[(j * 8 + m) * 32];
+                            const double r = rg[(j * 8 + 7) * 32];
+                            double acc = fwd_chain<EXACT>(r, L, w1, p1, p0, lw2, lw1, lp2, lp1);
+                            const bool bad = p_on && (is_sent(p0) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur))));
+                            if (__any_sync(0xffffffffu, bad)) {
+                                PLN_T0();
+                                long long spins = 0;
+                                for (;;) {
+                                    if (p_on && is_sent(p0)) p0 = gp_on ? ldg_cg(pw0 + tau * ZP)
+                                                                        : lds_vol(hin + ((tau + 1) & (HR - 1)) * 32);
+                                    if (gl_on && p_on) {
+                                        if (is_sent(ga_cur)) ga_cur = ldg_cg(pga + tau * ZP);
+                                        if (is_sent(gb_cur)) gb_cur = ldg_cg(pgb + tau * ZP);
+                                    }
+                                    const bool still =
+                                        p_on && (is_sent(p0) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur))));
+                                    if (!__any_sync(0xffffffffu, still)) break;
+                                    if (++spins > (1ll << 26)) __trap();
+                                }
+                                lw1 = gl_on ? ga_cur : lw1;
+                                lp1 = gl_on ? gb_cur : lp1;
+                                acc = fwd_chain<EXACT>(r, L, w1, p1, p0, lw2, lw1, lp2, lp1);
+                                PLN_ADD(4);
+                            }
+                            const bool vpt = tau >= lo && tau <= hi;
+                            const double wnew = vpt ? acc : 0.0;
+                            if (p_on && k > 0) sts(hin + ((tau + 1) & (HR - 1)) * 32, sentv());
+                            if (hout && tau >= T0 + 1) sts(hout + (tau & (HR - 1)) * 32, wnew);
+                            if (vpt) {
+                                pwo[tau * ZP] = wnew;
+                                if (rearm_b) pbo[tau * ZP] = sentv();
+                            }
+                            ga_prev = ga_cur; gb_prev = gb_cur;
+                            w2 = w1; w1 = wnew;
+                            p2 = p1; p1 = p0;
+                            prefetch(tau + PD);
+                        }
+                    }
+                    mb_arrive(&S.empty[k][sl]);
+                    ++seq;
+                };
+                for (int q = 0; q < ngroups; ++q) grp(q);
+                asm volatile("cp.async.wait_all;" ::: "memory");
             }
-        } else {
-            // ---- per-row state -------------------------------------------------------------
+        } else if (role == 1 && wlive) {
+            // ============================ march helper ==========================================
             double d[7][K];
             int boff = 0;
-            int64_t rbase = 0;
             if (live) {
                 const int r = row_id(n, z, y);
                 const double *sd = P.seedF + (int64_t)r * 7 * K;
@@ -336,265 +516,290 @@ __global__ void __launch_bounds__(PW * 32, 1) k_plane_fwd(const PlanDev P, const
 #pragma unroll
                     for (int j = 0; j < K; ++j) d[m][j] = sd[m * K + j];
                 if (P.variant == 1) boff = P.bandoff[r];
-                rbase = P.rowbase[r];
             } else {
 #pragma unroll
                 for (int m = 0; m < 7; ++m)
 #pragma unroll
                     for (int j = 0; j < K; ++j) d[m][j] = 0.0;
             }
-            // ---- TMA groups: group q stages steps sg = T0 + TG q .. + TG-1: one u box (planes s-1..s+1,
-            // lines sg0+1 .. sg0+TG+2) and one f box (lines sg0 .. sg0+TG-1) --------------------------
-            uint64_t *mb = S.mbar[warp];
-            const int ngroups = (T1 - T0) / TG + 1;
-            auto issue = [&](int q) {  // lane 0
-                const int sl = giss % NG;
-                const int sg0 = T0 + TG * q;
-                double *tb = reinterpret_cast<double *>(S.tbuf[warp][sl]);
-                mb_expect(&mb[sl], (3 * (TG + 2) + TG) * WIN * 8);
-                tma3(tb, &M.u3, z0 - 1, sg0 + 1, s - 1, &mb[sl]);
-                tma3(tb + FOFF, &M.f1, z0 - 1, sg0, s, &mb[sl]);
-                ++giss;
+            const bool v1 = P.variant == 1;
+            const bool rowband = z == 1 || y == 1;
+            // V1 band rows, loaded GS steps ahead: bl[j] = store row of step tq + j (when a band point)
+            auto band_ld = [&](int tau, double(&v)[7]) {
+                const bool isb = v1 && tau >= lo && tau <= hi && (rowband || tau == lo || tau == hi);
+                const int x = tau - z;
+                const double *st = P.store + 9 * (int64_t)(boff + (rowband ? x - 1 : (tau == lo ? 0 : 1)));
+#pragma unroll
+                for (int m = 0; m < 7; ++m) v[m] = ld_if(isb, st + m, 0.0);
+            };
+            double bl[GS][7];
+#pragma unroll
+            for (int j = 0; j < GS; ++j) band_ld(T0 + j, bl[j]);
+            for (int q = 0; q < ngroups; ++q, ++seq) {
+                const int sl = seq % NS;
+                const int tq = T0 + GS * q;
+                {
+                    PLN_T0();
+                    mb_wait(&S.empty[k][sl], ((seq / NS) & 1) ^ 1);
+                    PLN_ADD(2);
+                }
+                double *rg = &S.ring[k][sl][0][0][lane];
+#pragma unroll
+                for (int j = 0; j < GS; ++j) {
+                    const int tau = tq + j;
+                    const bool vpt = tau >= lo && tau <= hi;
+                    const bool isb = v1 && vpt && (rowband || tau == lo || tau == hi);
+#pragma unroll
+                    for (int m = 0; m < 7; ++m) rg[(j * 8 + m) * 32] = isb ? bl[j][m] : d[m][0];
+                    if (vpt) {
+#pragma unroll
+                        for (int m = 0; m < 7; ++m) march<K>(d[m]);
+                    }
+                    band_ld(tau + GS, bl[j]);
+                }
+                mb_arrive(&S.full[k][sl]);
+            }
+        } else if (role == 2 && wlive) {
+            // =========================== residual helper ========================================
+            int64_t rbase = 0;
+            if (live) rbase = P.rowbase[row_id(n, z, y)];
+            auto issue = [&](int q) {  // lane 0: u box (planes s-1..s+1, lines tq-2 .. tq+GS+1) + f box
+                const int sl = tiss % NT;
+                const int tq = T0 + GS * q;
+                double *tb = reinterpret_cast<double *>(S.tbuf[k][sl]);
+                mb_expect(&S.tfull[k][sl], (3 * (GS + 4) + GS) * WIN * 8);
+                tma3(tb, &M.u3, z0 - 1, tq - 2, s - 1, &S.tfull[k][sl]);
+                tma3(tb + FOFF, &M.f1, z0 - 1, tq, s, &S.tfull[k][sl]);
+                ++tiss;
             };
             if (lane == 0)
-                for (int q = 0; q < ngroups && q < NG; ++q) issue(q);
-            // ---- global handoff inputs, prefetched GS chain steps ahead ---------------------
-            // warp 0: P(tau+1) = w_f(s-1, tau+1, z); lane 0: ga = w_f(s, tau-1, z0-1), gb = w_f(s-1, tau, z0-1)
-            const double *pw0 = A.W + pidx(g, s - 1, 0, z);
-            const double *pga = A.W + pidx(g, s, 0, z0 - 1);
-            const double *pgb = A.W + pidx(g, s - 1, 0, z0 - 1);
-            const bool gp_on = (warp == 0), gl_on = (lane == 0);
-            double gp[GS], ga[GS], gb[GS];
-#pragma unroll
-            for (int j = 0; j < GS; ++j) {
-                const int tau = T0 + j;
-                gp[j] = (gp_on && tau + 1 >= 0) ? ldg_cg(pw0 + (int64_t)(tau + 1) * ZP) : 0.0;
-                ga[j] = (gl_on && tau - 1 >= 0) ? ldg_cg(pga + (int64_t)(tau - 1) * ZP) : 0.0;
-                gb[j] = (gl_on && tau >= 0) ? ldg_cg(pgb + (int64_t)tau * ZP) : 0.0;
-            }
-            // ---- sliding windows (residual of step sg) ----------------------------------------
-            double al0 = 0, al1 = 0, al2 = 0, al3 = 0, al4 = 0;  // u(s, sg+2-j, z-1)
-            double am0 = 0, am1 = 0, am2 = 0, am3 = 0;           // u(s, sg+2-j, z)
-            double ah0 = 0, ah1 = 0;                             // u(s, sg+2-j, z+1)
-            double bl0 = 0, bl1 = 0, bl2 = 0;                    // u(s-1, sg+1-j, z-1)
-            double bm0 = 0, bm1 = 0;                             // u(s-1, sg+1-j, z)
-            double cm0 = 0, cm1 = 0, cm2 = 0;                    // u(s+1, sg+1-j, z)
-            double ch0 = 0, ch1 = 0;                             // u(s+1, sg+1-j, z+1)
-            double rr_cur = 0.0;                                 // residual of the chain step
-            double w1 = 0, w2 = 0;                               // own w_f at tau-1, tau-2
-            double p1 = 0, p2 = 0;                               // w_f(s-1, tau, z), (s-1, tau-1, z)
-            double ga_prev = 0, gb_prev = 0;
-            long long cyc_slow = 0, cyc_wait = 0;
-            const bool rearm_b = live && (warp == 0 || (lane == 0 && z0 > 32));
-            const int i = lane + 1;
-            auto step = [&](const int sg, const int j) {
-                const int tau = sg - 1;
-                const int jc = (j + GS - 1) % GS;  // prefetch slot of chain step tau
-                const bool res_on = sg <= T1, chain_on = tau >= T0;
-                const bool p_on = chain_on && tau <= T1 - 1;
-                // (0) once per group: staged lines ready; the producer's next GS ring slots armed
-                const long long cw0 = A.trace ? clock64() : 0;
-                if (j == 0) {
-                    if (res_on && (sg - T0) % TG == 0) mb_wait(&mb[gcon % NG], (gcon / NG) & 1);
-                    if (hout) {
-                        long long spins = 0;
-                        for (;;) {
-                            bool busy = false;
-#pragma unroll
-                            for (int k = 0; k < GS; ++k) {
-                                const int tt = tau + k;
-                                if (tt >= T0 + 1 && tt <= T1) busy |= !is_sent(lds_vol(hout + hs(tt) + lane));
-                            }
-                            if (!__any_sync(0xffffffffu, busy)) break;
-                            if (++spins > (1ll << 28)) __trap();
-                        }
-                    }
-                }
-                if (A.trace) cyc_wait += clock64() - cw0;
-                // (1) chain inputs, taken speculatively
-                double p0 = 0.0;
-                if (p_on) p0 = (warp == 0) ? gp[jc] : lds_vol(hin + hs(tau + 1) + lane);
-                double ga_cur = ga[jc], gb_cur = gb[jc];
-                double lw1 = __shfl_up_sync(0xffffffffu, w1, 1);
-                double lw2 = __shfl_up_sync(0xffffffffu, w2, 1);
-                double lp1 = __shfl_up_sync(0xffffffffu, p1, 1);
-                double lp2 = __shfl_up_sync(0xffffffffu, p2, 1);
-                if (lane == 0) {
-                    lw1 = ga_cur; lw2 = ga_prev; lp1 = gb_cur; lp2 = gb_prev;
-                }
-                const int x = tau - z;
-                const bool vpt = chain_on && live && x >= 1 && x <= xe;
-                double L[7];
+                for (int q = 0; q < ngroups && q < NT; ++q) issue(q);
+            for (int q = 0; q < ngroups; ++q, ++seq, ++tseq) {
+                const int sl = seq % NS, tsl = tseq % NT;
+                const int tq = T0 + GS * q;
                 {
-                    const bool isb = (P.variant == 1) && vpt && band_pt(x, y, z, xe);
-                    const double *st = P.store + 9 * (int64_t)(boff + band_off(x, y, z));
-#pragma unroll
-                    for (int m = 0; m < 7; ++m) L[m] = ld_if(isb, st + m, d[m][0]);
+                    PLN_T0();
+                    mb_wait(&S.tfull[k][tsl], (tseq / NT) & 1);
+                    PLN_ADD(3);
                 }
-                // (2) residual of step sg (independent of the chain)
-                double rr_next = 0.0;
-                if (res_on) {
-                    const int k = (sg - T0) % TG;
-                    const double *tb = reinterpret_cast<const double *>(S.tbuf[warp][gcon % NG]);
-                    const double *la = tb + ((TG + 2) + k + 1) * WIN;      // u(s, sg+2)
-                    const double *lb = tb + k * WIN;                       // u(s-1, sg+1)
-                    const double *lc = tb + (2 * (TG + 2) + k) * WIN;      // u(s+1, sg+1)
-                    const double *lf = tb + FOFF + k * WIN;                // f(s, sg)
-                    al4 = al3; al3 = al2; al2 = al1; al1 = al0; al0 = la[i - 1];
-                    am3 = am2; am2 = am1; am1 = am0; am0 = la[i];
-                    ah1 = ah0; ah0 = la[i + 1];
-                    bl2 = bl1; bl1 = bl0; bl0 = lb[i - 1];
-                    bm1 = bm0; bm0 = lb[i];
-                    cm2 = cm1; cm1 = cm0; cm0 = lc[i];
-                    ch1 = ch0; ch0 = lc[i + 1];
-                    const double fv = lf[i];
-                    const int xs = sg - z;
-                    if (live && xs >= 1 && xs <= xe) {
+                {
+                    PLN_T0();
+                    mb_wait(&S.empty[k][sl], ((seq / NS) & 1) ^ 1);
+                    PLN_ADD(2);
+                }
+                double *rg = &S.ring[k][sl][0][0][lane];
+#pragma unroll
+                for (int j = 0; j < GS; ++j) {
+                    const int sg = tq + j;
+                    const double *tb = reinterpret_cast<const double *>(S.tbuf[k][tsl]) + j * WIN + lane + 1;
+                    const double *u1 = tb + (GS + 4) * WIN;      // plane s,   line sg-2 at offset 0
+                    const double *u0 = tb;                       // plane s-1
+                    const double *u2 = tb + 2 * (GS + 4) * WIN;  // plane s+1
+                    constexpr int Wn = WIN;
+                    double res = 0.0;
+                    if (sg >= lo && sg <= hi) {
                         double a[15];
                         if (CONST_ROW) {
 #pragma unroll
-                            for (int q = 0; q < 15; ++q) a[q] = A.arow[q];
+                            for (int qq = 0; qq < 15; ++qq) a[qq] = A.arow[qq];
                         } else {
-                            const double *ar = P.arows + 15 * (rbase + xs);
+                            const double *ar = P.arows + 15 * (rbase + (sg - z));
 #pragma unroll
-                            for (int q = 0; q < 15; ++q) a[q] = ar[q];
+                            for (int qq = 0; qq < 15; ++qq) a[qq] = ar[qq];
                         }
                         // stencil_apply order (_kernels.py:243-267): c, w s se bnw bn bc be, e n nw tse ts tc tw
-                        double out = EXACT ? dmul(a[7], am2) : a[7] * am2;
-                        out = madd<EXACT>(out, a[0], am3);
-                        out = madd<EXACT>(out, a[1], bm1);
-                        out = madd<EXACT>(out, a[2], bm0);
-                        out = madd<EXACT>(out, a[3], al4);
-                        out = madd<EXACT>(out, a[4], al3);
-                        out = madd<EXACT>(out, a[5], bl2);
-                        out = madd<EXACT>(out, a[6], bl1);
-                        out = madd<EXACT>(out, a[8], am1);
-                        out = madd<EXACT>(out, a[9], cm1);
-                        out = madd<EXACT>(out, a[10], cm2);
-                        out = madd<EXACT>(out, a[11], ah0);
-                        out = madd<EXACT>(out, a[12], ah1);
-                        out = madd<EXACT>(out, a[13], ch0);
-                        out = madd<EXACT>(out, a[14], ch1);
-                        rr_next = dsub(fv, out);
-                        r2 = fma(rr_next, rr_next, r2);
+                        double out = EXACT ? dmul(a[7], u1[2 * Wn]) : a[7] * u1[2 * Wn];
+                        out = madd<EXACT>(out, a[0], u1[1 * Wn]);        // w   (s,   sg-1, z)
+                        out = madd<EXACT>(out, a[1], u0[2 * Wn]);        // s   (s-1, sg,   z)
+                        out = madd<EXACT>(out, a[2], u0[3 * Wn]);        // se  (s-1, sg+1, z)
+                        out = madd<EXACT>(out, a[3], u1[0 * Wn - 1]);    // bnw (s,   sg-2, z-1)
+                        out = madd<EXACT>(out, a[4], u1[1 * Wn - 1]);    // bn  (s,   sg-1, z-1)
+                        out = madd<EXACT>(out, a[5], u0[1 * Wn - 1]);    // bc  (s-1, sg-1, z-1)
+                        out = madd<EXACT>(out, a[6], u0[2 * Wn - 1]);    // be  (s-1, sg,   z-1)
+                        out = madd<EXACT>(out, a[8], u1[3 * Wn]);        // e   (s,   sg+1, z)
+                        out = madd<EXACT>(out, a[9], u2[2 * Wn]);        // n   (s+1, sg,   z)
+                        out = madd<EXACT>(out, a[10], u2[1 * Wn]);       // nw  (s+1, sg-1, z)
+                        out = madd<EXACT>(out, a[11], u1[4 * Wn + 1]);   // tse (s,   sg+2, z+1)
+                        out = madd<EXACT>(out, a[12], u1[3 * Wn + 1]);   // ts  (s,   sg+1, z+1)
+                        out = madd<EXACT>(out, a[13], u2[3 * Wn + 1]);   // tc  (s+1, sg+1, z+1)
+                        out = madd<EXACT>(out, a[14], u2[2 * Wn + 1]);   // tw  (s+1, sg,   z+1)
+                        res = dsub(tb[FOFF], out);
+                        r2 = fma(res, res, r2);
                     }
+                    rg[(j * 8 + 7) * 32] = res;
                 }
-                // (3) substitution of step tau
-                double acc = fwd_chain<EXACT>(rr_cur, L, w1, p1, p0, lw2, lw1, lp2, lp1);
-                // (4) validate the speculative inputs
-                const bool bad = p_on && (is_sent(p0) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur))));
-                if (__any_sync(0xffffffffu, bad)) {
-                    const long long cs0 = A.trace ? clock64() : 0;
-                    long long spins = 0;
-                    for (;;) {
-                        if (p_on && is_sent(p0)) p0 = (warp == 0) ? ldg_cg(pw0 + (int64_t)(tau + 1) * ZP)
-                                                                  : lds_vol(hin + hs(tau + 1) + lane);
-                        if (gl_on && p_on) {
-                            if (is_sent(ga_cur)) ga_cur = ldg_cg(pga + (int64_t)(tau - 1) * ZP);
-                            if (is_sent(gb_cur)) gb_cur = ldg_cg(pgb + (int64_t)tau * ZP);
-                        }
-                        const bool still = p_on && (is_sent(p0) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur))));
-                        if (!__any_sync(0xffffffffu, still)) break;
-                        __nanosleep(32);
-                        if (++spins > (1ll << 26)) __trap();
-                    }
-                    if (lane == 0) {
-                        lw1 = ga_cur; lp1 = gb_cur;
-                    }
-                    acc = fwd_chain<EXACT>(rr_cur, L, w1, p1, p0, lw2, lw1, lp2, lp1);
-                    if (A.trace) cyc_slow += clock64() - cs0;
-                }
-                const double wnew = vpt ? acc : 0.0;
-                // (5) publish
-                if (p_on && warp > 0) sts(hin + hs(tau + 1) + lane, sentv());   // re-arm the consumed slot
-                if (hout && chain_on && tau >= T0 + 1) sts(hout + hs(tau) + lane, wnew);
-                if (vpt) {
-                    const int64_t pi = pidx(g, s, tau, z);
-                    A.W[pi] = wnew;
-                    if (rearm_b) A.B[pi] = sentv();
-#pragma unroll
-                    for (int m = 0; m < 7; ++m) march<K>(d[m]);
-                }
-                if (chain_on) {
-                    ga_prev = ga_cur; gb_prev = gb_cur;
-                    w2 = w1; w1 = wnew;
-                    p2 = p1; p1 = p0;
-                    // prefetch the global inputs of chain step tau + GS
-                    const int tn = tau + GS;
-                    if (gp_on) gp[jc] = ldg_cg(pw0 + (int64_t)(tn + 1) * ZP);
-                    if (gl_on) {
-                        ga[jc] = ldg_cg(pga + (int64_t)(tn - 1) * ZP);
-                        gb[jc] = ldg_cg(pgb + (int64_t)tn * ZP);
-                    }
-                }
-                rr_cur = rr_next;
-                // (6) end of a staged group: release the slot, stage group + NG
-                if (res_on && ((sg - T0) % TG == TG - 1 || sg == T1)) {
-                    __syncwarp();
-                    const int q = (sg - T0) / TG;
-                    ++gcon;
-                    if (lane == 0 && q + NG < ngroups) issue(q + NG);
-                }
-            };
-            const long long ct0 = A.trace ? clock64() : 0;
-            for (int sg0 = T0; sg0 <= T1 + 1; sg0 += GS) {
-#pragma unroll
-                for (int j = 0; j < GS; ++j)
-                    if (sg0 + j <= T1 + 1) step(sg0 + j, j);
-            }
-            if (A.trace && lane == 0) {
-                long long *tr = A.trace + TR * (int64_t)t + 4 + 3 * warp;
-                tr[0] = clock64() - ct0;
-                tr[1] = cyc_slow;
-                tr[2] = cyc_wait;
+                __syncwarp();
+                if (lane == 0 && q + NT < ngroups) issue(q + NT);
+                mb_arrive(&S.full[k][sl]);
             }
         }
-        if (A.part) A.part[(int64_t)t * (PW * 32) + threadIdx.x] = r2;
+        if (A.part && role == 2) A.part[(int64_t)t * (PW * 32) + k * 32 + lane] = r2;
+#ifdef TILU_PLANE_PROF
+        if (prof && lane == 0) {
+            long long *sl = A.steplog + wid * 8;
+            sl[0] += clock64() - pstart;
+            for (int i = 1; i < 5; ++i) sl[i] += pc[i];
+            sl[5] += ngroups;
+        }
+#endif
         __syncthreads();
-        if (A.trace && threadIdx.x == 0) {
-            A.trace[TR * (int64_t)t + 1] = gtimer();
-            A.trace[TR * (int64_t)t + 2] = smid();
-            A.trace[TR * (int64_t)t + 3] = blockIdx.x;
-        }
+        trace_end(A, t);
     }
 }
 
 // ------------------------------------------------------------------------------------------------
 // Backward pass: D^{-1} scaling + L^T substitution (descending), fused u += w (multigrid.py:429).
+// Per diagonal two warps: the solver (role 0: substitution, handoffs, TMA of w_f and u) and the
+// march helper (role 1: the seven source-point L values and 1/D of every point, V1 band rows).
 // ------------------------------------------------------------------------------------------------
 template <int K, bool EXACT>
-__global__ void __launch_bounds__(PW * 32, 1) k_plane_bwd(const PlanDev P, const Args A, const __grid_constant__ Maps M)
+__global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, const Args A, const __grid_constant__ Maps M)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    init_smem(S);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k = wid % PW, role = wid / PW;
+    init_smem<1>(S);
     const Geo g = A.g;
     const int n = P.n, ZP = g.ZP;
-    uint32_t gcon = 0, giss = 0;
+    uint32_t seq = 0, tseq = 0, tiss = 0;
     for (;;) {
         if (threadIdx.x == 0) S.task = atomicAdd(A.ticket, 1);
         __syncthreads();
         const int t = S.task;
         if (t >= A.ntasks) break;
+        trace_start(A, t);
         const int code = A.tasks[A.ntasks - 1 - t];
         const int b = code >> 16, c = code & 0xffff;
-        if (A.trace && threadIdx.x == 0) A.trace[TR * (int64_t)t] = gtimer();
         const int s0 = 2 + PW * b, z0 = 1 + 32 * c;
-        const int s = s0 + PW - 1 - warp, z = z0 + lane, y = s - z;
+        const int s = s0 + PW - 1 - k, z = z0 + lane, y = s - z;
         const int xe = n - 1 - s, xe0 = n - 1 - s0;
-        const int T0 = z0 - 1, T1 = z0 + 32 + xe0;  // loop tau = T1 .. T0-1 (descending)
+        const int T0 = z0 - 1, T1 = z0 + 32 + xe0;  // steps tau = T1 .. T0-1 (descending)
         const bool wlive = (s <= n - 2) && (z0 <= s - 1);
         const bool live = wlive && (z <= s - 1);
-        double *hin = &S.hring[warp][0][0];
-        double *hout = (warp + 1 < PW) ? &S.hring[warp + 1][0][0] : nullptr;
-        auto hs = [](int tau) { return ((tau + HR) % HR) * 32; };
-        if (!wlive) {
-            for (int tau = T1; tau >= T0 - 1; --tau) {
-                if (warp > 0 && tau >= T0) (void)take_s(hin + hs(tau - 1) + lane);
-                if (hout && tau <= T1 - 1) put_s(hout + hs(tau) + lane, 0.0);
+        const int lo = live ? z + 1 : 1 << 30, hi = live ? z + xe : -(1 << 30);
+        const int ngroups = (T1 - (T0 - 1)) / GS + 1;
+        if (role == 0) {
+            double *hin = &S.hring[k][0][lane];
+            double *hout = (k + 1 < PW) ? &S.hring[k + 1][0][lane] : nullptr;
+            if (!wlive) {
+                for (int tau = T1; tau >= T0 - 1; --tau) {
+                    if (k > 0 && tau >= T0) (void)take_s(hin + ((tau - 1) & (HR - 1)) * 32);
+                    if (hout && tau <= T1 - 1) put_s(hout + (tau & (HR - 1)) * 32, 0.0);
+                }
+            } else {
+                // group q stages tau = T1 - GS q .. T1 - GS q - (GS-1): w_f and u boxes of GS lines
+                auto issue = [&](int q) {
+                    const int sl = tiss % NT;
+                    const int lo_t = T1 - GS * q - (GS - 1);
+                    double *tb = reinterpret_cast<double *>(S.tbuf[k][sl]);
+                    mb_expect(&S.tfull[k][sl], 2 * GS * WIN * 8);
+                    tma3(tb, &M.w1, z0 - 1, lo_t, s, &S.tfull[k][sl]);
+                    tma3(tb + UOFF, &M.u1, z0 - 1, lo_t, s, &S.tfull[k][sl]);
+                    ++tiss;
+                };
+                if (lane == 0)
+                    for (int q = 0; q < ngroups && q < NT; ++q) issue(q);
+                // warp 0: P'(tau-1) = w_b(s+1, tau-1, z); lane 31: ga = w_b(s, tau+1, z0+32), gb = w_b(s+1, tau, z0+32)
+                const double *pw0 = A.B + pidx(g, s + 1, -1, z);
+                const double *pga = A.B + pidx(g, s, 1, z0 + 32);
+                const double *pgb = A.B + pidx(g, s + 1, 0, z0 + 32);
+                double *puo = A.u + pidx(g, s, 0, z);
+                double *pbo = A.B + pidx(g, s, 0, z);
+                double *pwo = A.W + pidx(g, s, 0, z);
+                const bool gp_on = (k == 0), gl_on = (lane == 31);
+                double *pre = &S.pre[k][0][0][lane];
+                auto prefetch = [&](int tau) {
+                    double *d = pre + (tau & (PD - 1)) * 96;
+                    if (gp_on) cpa8(d, pw0 + tau * ZP);
+                    if (gl_on) {
+                        cpa8(d + 32, pga + tau * ZP);
+                        cpa8(d + 64, pgb + tau * ZP);
+                    }
+                    cpa_commit();
+                };
+                for (int i = 0; i < PD; ++i) prefetch(T1 - i);
+                double wb1 = 0, wb2 = 0, q1 = 0, q2 = 0, ga_prev = 0, gb_prev = 0;
+                const bool b_out = live && (k == PW - 1 || (lane == 0 && z0 > 32));
+                const bool rearm_w = live && (k == 0 || lane == 31);
+                auto grp = [&](const int q) {
+                    const int sl = seq % NS, tsl = tseq % NT;
+                    const int tq = T1 - GS * q;
+                    if (hout) wait_armed(hout, tq, -1, T0 - 1, T1 - 1);
+                    mb_wait(&S.tfull[k][tsl], (tseq / NT) & 1);
+                    mb_wait(&S.full[k][sl], (seq / NS) & 1);
+                    const double *rg = &S.ring[k][sl][0][0][lane];
+                    const double *tb = reinterpret_cast<const double *>(S.tbuf[k][tsl]) + lane + 1;
+#pragma unroll
+                    for (int j = 0; j < GS; ++j) {
+                        const int tau = tq - j;
+                        if (tau >= T0 - 1) {
+                            const bool q_on = tau >= T0;
+                            double q0 = 0.0;
+                            cpa_wait_pd();
+                            const double *pv = pre + (tau & (PD - 1)) * 96;
+                            if (q_on) q0 = gp_on ? pv[0] : lds_vol(hin + ((tau - 1) & (HR - 1)) * 32);
+                            double ga_cur = pv[32], gb_cur = pv[64];
+                            double lw1 = __shfl_down_sync(0xffffffffu, wb1, 1);
+                            double lw2 = __shfl_down_sync(0xffffffffu, wb2, 1);
+                            double lq1 = __shfl_down_sync(0xffffffffu, q1, 1);
+                            double lq2 = __shfl_down_sync(0xffffffffu, q2, 1);
+                            lw1 = gl_on ? ga_cur : lw1;
+                            lw2 = gl_on ? ga_prev : lw2;
+                            lq1 = gl_on ? gb_cur : lq1;
+                            lq2 = gl_on ? gb_prev : lq2;
+                            const double wfv = tb[(GS - 1 - j) * WIN];          // line of tau in the boxes
+                            const double uv = tb[UOFF + (GS - 1 - j) * WIN];
+                            double Lq[7];
+#pragma unroll
+                            for (int m = 0; m < 7; ++m) Lq[m] = rg[(j * 8 + m) * 32];
+                            const double inv_d = rg[(j * 8 + 7) * 32];
+                            double acc = bwd_chain<EXACT>(inv_d, wfv, Lq, wb1, q1, q0, lw2, lw1, lq2, lq1);
+                            const bool bad = (q_on && is_sent(q0)) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur)));
+                            if (__any_sync(0xffffffffu, bad)) {
+                                long long spins = 0;
+                                for (;;) {
+                                    if (q_on && is_sent(q0)) q0 = gp_on ? ldg_cg(pw0 + tau * ZP)
+                                                                        : lds_vol(hin + ((tau - 1) & (HR - 1)) * 32);
+                                    if (gl_on) {
+                                        if (is_sent(ga_cur)) ga_cur = ldg_cg(pga + tau * ZP);
+                                        if (is_sent(gb_cur)) gb_cur = ldg_cg(pgb + tau * ZP);
+                                    }
+                                    const bool still =
+                                        (q_on && is_sent(q0)) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur)));
+                                    if (!__any_sync(0xffffffffu, still)) break;
+                                    if (++spins > (1ll << 26)) __trap();
+                                }
+                                lw1 = gl_on ? ga_cur : lw1;
+                                lq1 = gl_on ? gb_cur : lq1;
+                                acc = bwd_chain<EXACT>(inv_d, wfv, Lq, wb1, q1, q0, lw2, lw1, lq2, lq1);
+                            }
+                            const bool vpt = tau >= lo && tau <= hi;
+                            const double wnew = vpt ? acc : 0.0;
+                            if (q_on && k > 0) sts(hin + ((tau - 1) & (HR - 1)) * 32, sentv());
+                            if (hout && tau <= T1 - 1) sts(hout + (tau & (HR - 1)) * 32, wnew);
+                            if (vpt) {
+                                puo[tau * ZP] = dadd(uv, acc);
+                                if (b_out) pbo[tau * ZP] = acc;
+                                if (rearm_w) pwo[tau * ZP] = sentv();
+                            }
+                            ga_prev = ga_cur; gb_prev = gb_cur;
+                            wb2 = wb1; wb1 = wnew;
+                            q2 = q1; q1 = q0;
+                            prefetch(tau - PD);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0 && q + NT < ngroups) issue(q + NT);
+                    mb_arrive(&S.empty[k][sl]);
+                    ++seq;
+                    ++tseq;
+                };
+                for (int q = 0; q < ngroups; ++q) grp(q);
+                asm volatile("cp.async.wait_all;" ::: "memory");
             }
-        } else {
+        } else if (wlive) {
+            // ============================ march helper ==========================================
             double d[8][K];
             int bo_own = 0, bo_n = 0, bo_ts = 0, bo_tc = 0;
             if (live) {
@@ -618,180 +823,69 @@ __global__ void __launch_bounds__(PW * 32, 1) k_plane_bwd(const PlanDev P, const
 #pragma unroll
                     for (int j = 0; j < K; ++j) d[m][j] = 0.0;
             }
-            uint64_t *mb = S.mbar[warp];
-            // group q stages tau = T1 - TG q down to T1 - TG q - (TG-1): w_f and u boxes of TG lines
-            const int ngroups = (T1 - (T0 - 1)) / TG + 1;
-            auto issue = [&](int q) {
-                const int sl = giss % NG;
-                const int lo = T1 - TG * q - (TG - 1);
-                double *tb = reinterpret_cast<double *>(S.tbuf[warp][sl]);
-                mb_expect(&mb[sl], 2 * TG * WIN * 8);
-                tma3(tb, &M.w1, z0 - 1, lo, s, &mb[sl]);
-                tma3(tb + TG * WIN, &M.u1, z0 - 1, lo, s, &mb[sl]);
-                ++giss;
-            };
-            if (lane == 0)
-                for (int q = 0; q < ngroups && q < NG; ++q) issue(q);
-            // warp 0: P'(tau-1) = w_b(s+1, tau-1, z); lane 31: ga = w_b(s, tau+1, z0+32), gb = w_b(s+1, tau, z0+32)
-            const double *pw0 = A.B + pidx(g, s + 1, 0, z);
-            const double *pga = A.B + pidx(g, s, 0, z0 + 32);
-            const double *pgb = A.B + pidx(g, s + 1, 0, z0 + 32);
-            const bool gp_on = (warp == 0), gl_on = (lane == 31);
-            double gp[GS], ga[GS], gb[GS];
-#pragma unroll
-            for (int j = 0; j < GS; ++j) {
-                const int tau = T1 - j;
-                gp[j] = (gp_on && tau - 1 >= 0) ? ldg_cg(pw0 + (int64_t)(tau - 1) * ZP) : 0.0;
-                ga[j] = gl_on ? ldg_cg(pga + (int64_t)(tau + 1) * ZP) : 0.0;
-                gb[j] = gl_on ? ldg_cg(pgb + (int64_t)tau * ZP) : 0.0;
-            }
-            double wb1 = 0, wb2 = 0;  // own w_b at tau+1, tau+2
-            double q1 = 0, q2 = 0;    // w_b(s+1, tau, z), (s+1, tau+1, z)
-            double ga_prev = 0, gb_prev = 0;
-            long long cyc_slow = 0, cyc_wait = 0;
-            const bool b_out = live && (warp == PW - 1 || (lane == 0 && z0 > 32));
-            const bool rearm_w = live && (warp == 0 || lane == 31);
-            const int i = lane + 1;
-            auto step = [&](const int tau, const int j) {
-                const bool q_on = tau >= T0;
-                const long long cw0 = A.trace ? clock64() : 0;
-                if (j == 0) {
-                    if ((T1 - tau) % TG == 0) mb_wait(&mb[gcon % NG], (gcon / NG) & 1);
-                    if (hout) {
-                        long long spins = 0;
-                        for (;;) {
-                            bool busy = false;
-#pragma unroll
-                            for (int k = 0; k < GS; ++k) {
-                                const int tt = tau - k;
-                                if (tt <= T1 - 1 && tt >= T0 - 1) busy |= !is_sent(lds_vol(hout + hs(tt) + lane));
-                            }
-                            if (!__any_sync(0xffffffffu, busy)) break;
-                            if (++spins > (1ll << 28)) __trap();
-                        }
-                    }
-                }
-                if (A.trace) cyc_wait += clock64() - cw0;
-                double q0 = 0.0;
-                if (q_on) q0 = (warp == 0) ? gp[j] : lds_vol(hin + hs(tau - 1) + lane);
-                double ga_cur = ga[j], gb_cur = gb[j];
-                double lw1 = __shfl_down_sync(0xffffffffu, wb1, 1);
-                double lw2 = __shfl_down_sync(0xffffffffu, wb2, 1);
-                double lq1 = __shfl_down_sync(0xffffffffu, q1, 1);
-                double lq2 = __shfl_down_sync(0xffffffffu, q2, 1);
-                if (lane == 31) {
-                    lw1 = ga_cur; lw2 = ga_prev; lq1 = gb_cur; lq2 = gb_prev;
-                }
+            const bool v1 = P.variant == 1;
+            const bool zr1 = z == 1, yr1 = y == 1, yr2 = y == 2, yge2 = y >= 2;
+            // band / interior tests of the seven source points q_m = p - d_m (_lq, _kernels.py:434-441)
+            // and of p (1/D).  Masks: bit m = q_m interior (m < 7); band bits in bmask (bit 7 = p).
+            auto tests = [&](int tau, unsigned &imask, unsigned &bmask, int (&o)[8]) {
                 const int x = tau - z;
-                const bool vpt = live && x >= 1 && x <= xe;
-                double wfv, uv;
-                {
-                    const int k = TG - 1 - (T1 - tau) % TG;  // line of tau in the group's boxes
-                    const double *tb = reinterpret_cast<const double *>(S.tbuf[warp][gcon % NG]);
-                    wfv = tb[k * WIN + i];
-                    uv = tb[(TG + k) * WIN + i];
+                const bool vpt = tau >= lo && tau <= hi;
+                const bool x1 = x == 1, x2 = x == 2, xm1 = x == xe - 1, xm0 = x == xe;
+                const bool i0 = x + 1 <= xe, i1 = x <= xe - 1, i2 = x >= 2, i3 = yge2 && x + 1 <= xe;
+                imask = (unsigned)i0 | (unsigned)i1 << 1 | (unsigned)i2 << 2 | (unsigned)i3 << 3 |
+                        (unsigned)yge2 << 4 | (unsigned)i1 << 5 | (unsigned)i2 << 6;
+                bmask = 0;
+                if (v1 && vpt) {
+                    bmask = (unsigned)(i0 && (xm1 || yr1 || zr1)) | (unsigned)(i1 && (x1 || xm1 || zr1)) << 1 |
+                            (unsigned)(i2 && (x2 || xm0 || zr1)) << 2 | (unsigned)(i3 && (xm1 || yr2)) << 3 |
+                            (unsigned)(yge2 && (x1 || xm0 || yr2)) << 4 | (unsigned)(i1 && (x1 || xm1 || yr1)) << 5 |
+                            (unsigned)(i2 && (x2 || xm0 || yr1)) << 6 | (unsigned)(x1 || xm0 || yr1 || zr1) << 7;
                 }
-                // L at the seven source points q_m = p - d_m (_lq, _kernels.py:434-441) and 1/D at p
-                double Lq[7], inv_d;
-                {
-                    const bool v1 = P.variant == 1 && vpt;
-                    const bool i0 = x + 1 <= xe, i1 = x <= xe - 1, i2 = x >= 2, i3 = y >= 2 && x + 1 <= xe,
-                               i4 = y >= 2, i5 = x <= xe - 1, i6 = x >= 2;
-                    const bool b0 = v1 && i0 && (x + 1 == xe || y == 1 || z == 1);
-                    const bool b1 = v1 && i1 && (x == 1 || x == xe - 1 || z == 1);
-                    const bool b2 = v1 && i2 && (x - 1 == 1 || x - 1 == xe - 1 || z == 1);
-                    const bool b3 = v1 && i3 && (x + 1 == xe || y == 2);
-                    const bool b4 = v1 && i4 && (x == 1 || x == xe || y == 2);
-                    const bool b5 = v1 && i5 && (x == 1 || x == xe - 1 || y == 1);
-                    const bool b6 = v1 && i6 && (x - 1 == 1 || x - 1 == xe - 1 || y == 1);
-                    const bool bd = v1 && (x == 1 || x == xe || y == 1 || z == 1);
-                    const double *st = P.store;
-                    const int o0 = bo_own + ((z == 1 || y == 1) ? x : 1);
-                    const int o1 = bo_n + ((z == 1) ? x - 1 : (x == 1 ? 0 : 1));
-                    const int o2 = bo_n + ((z == 1) ? x - 2 : (x - 1 == 1 ? 0 : 1));
-                    const int o3 = bo_ts + ((y == 2) ? x : 1);
-                    const int o4 = bo_ts + ((y == 2) ? x - 1 : (x == 1 ? 0 : 1));
-                    const int o5 = bo_tc + ((y == 1) ? x - 1 : (x == 1 ? 0 : 1));
-                    const int o6 = bo_tc + ((y == 1) ? x - 2 : (x - 1 == 1 ? 0 : 1));
-                    const int od = bo_own + band_off(x, y, z);
-                    Lq[0] = i0 ? ld_if(b0, st + 9 * (int64_t)o0 + 0, d[0][0]) : 0.0;
-                    Lq[1] = i1 ? ld_if(b1, st + 9 * (int64_t)o1 + 1, d[1][0]) : 0.0;
-                    Lq[2] = i2 ? ld_if(b2, st + 9 * (int64_t)o2 + 2, d[2][0]) : 0.0;
-                    Lq[3] = i3 ? ld_if(b3, st + 9 * (int64_t)o3 + 3, d[3][0]) : 0.0;
-                    Lq[4] = i4 ? ld_if(b4, st + 9 * (int64_t)o4 + 4, d[4][0]) : 0.0;
-                    Lq[5] = i5 ? ld_if(b5, st + 9 * (int64_t)o5 + 5, d[5][0]) : 0.0;
-                    Lq[6] = i6 ? ld_if(b6, st + 9 * (int64_t)o6 + 6, d[6][0]) : 0.0;
-                    inv_d = ld_if(bd, st + 9 * (int64_t)od + 8, d[7][0]);
-                }
-                double acc = bwd_chain<EXACT>(inv_d, wfv, Lq, wb1, q1, q0, lw2, lw1, lq2, lq1);
-                const bool bad = (q_on && is_sent(q0)) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur)));
-                if (__any_sync(0xffffffffu, bad)) {
-                    const long long cs0 = A.trace ? clock64() : 0;
-                    long long spins = 0;
-                    for (;;) {
-                        if (q_on && is_sent(q0)) q0 = (warp == 0) ? ldg_cg(pw0 + (int64_t)(tau - 1) * ZP)
-                                                                  : lds_vol(hin + hs(tau - 1) + lane);
-                        if (gl_on) {
-                            if (is_sent(ga_cur)) ga_cur = ldg_cg(pga + (int64_t)(tau + 1) * ZP);
-                            if (is_sent(gb_cur)) gb_cur = ldg_cg(pgb + (int64_t)tau * ZP);
-                        }
-                        const bool still = (q_on && is_sent(q0)) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur)));
-                        if (!__any_sync(0xffffffffu, still)) break;
-                        __nanosleep(32);
-                        if (++spins > (1ll << 26)) __trap();
-                    }
-                    if (lane == 31) {
-                        lw1 = ga_cur; lq1 = gb_cur;
-                    }
-                    acc = bwd_chain<EXACT>(inv_d, wfv, Lq, wb1, q1, q0, lw2, lw1, lq2, lq1);
-                    if (A.trace) cyc_slow += clock64() - cs0;
-                }
-                const double wnew = vpt ? acc : 0.0;
-                if (q_on && warp > 0) sts(hin + hs(tau - 1) + lane, sentv());
-                if (hout && tau <= T1 - 1) sts(hout + hs(tau) + lane, wnew);
-                if (vpt) {
-                    const int64_t pi = pidx(g, s, tau, z);
-                    A.u[pi] = dadd(uv, acc);
-                    if (b_out) A.B[pi] = acc;
-                    if (rearm_w) A.W[pi] = sentv();
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) march<K>(d[m]);
-                }
-                ga_prev = ga_cur; gb_prev = gb_cur;
-                wb2 = wb1; wb1 = wnew;
-                q2 = q1; q1 = q0;
-                const int tn = tau - GS;
-                if (gp_on) gp[j] = (tn - 1 >= 0) ? ldg_cg(pw0 + (int64_t)(tn - 1) * ZP) : 0.0;
-                if (gl_on) {
-                    ga[j] = (tn + 1 >= 0) ? ldg_cg(pga + (int64_t)(tn + 1) * ZP) : 0.0;
-                    gb[j] = (tn >= 0) ? ldg_cg(pgb + (int64_t)tn * ZP) : 0.0;
-                }
-                if ((T1 - tau) % TG == TG - 1 || tau == T0 - 1) {
-                    __syncwarp();
-                    const int q = (T1 - tau) / TG;
-                    ++gcon;
-                    if (lane == 0 && q + NG < ngroups) issue(q + NG);
-                }
+                o[0] = bo_own + ((zr1 || yr1) ? x : 1);
+                o[1] = bo_n + (zr1 ? x - 1 : (x1 ? 0 : 1));
+                o[2] = bo_n + (zr1 ? x - 2 : (x2 ? 0 : 1));
+                o[3] = bo_ts + (yr2 ? x : 1);
+                o[4] = bo_ts + (yr2 ? x - 1 : (x1 ? 0 : 1));
+                o[5] = bo_tc + (yr1 ? x - 1 : (x1 ? 0 : 1));
+                o[6] = bo_tc + (yr1 ? x - 2 : (x2 ? 0 : 1));
+                o[7] = bo_own + ((zr1 || yr1) ? x - 1 : (x1 ? 0 : 1));
             };
-            const long long ct0 = A.trace ? clock64() : 0;
-            for (int t0 = T1; t0 >= T0 - 1; t0 -= GS) {
+            auto band_ld = [&](int tau, double(&v)[8]) {
+                unsigned im, bm;
+                int o[8];
+                tests(tau, im, bm, o);
 #pragma unroll
-                for (int j = 0; j < GS; ++j)
-                    if (t0 - j >= T0 - 1) step(t0 - j, j);
-            }
-            if (A.trace && lane == 0) {
-                long long *tr = A.trace + TR * (int64_t)t + 4 + 3 * warp;
-                tr[0] = clock64() - ct0;
-                tr[1] = cyc_slow;
-                tr[2] = cyc_wait;
+                for (int m = 0; m < 8; ++m) v[m] = ld_if((bm >> m) & 1u, P.store + 9 * (int64_t)o[m] + (m < 7 ? m : 8), 0.0);
+            };
+            double bl[GS][8];
+#pragma unroll
+            for (int j = 0; j < GS; ++j) band_ld(T1 - j, bl[j]);
+            for (int q = 0; q < ngroups; ++q, ++seq) {
+                const int sl = seq % NS;
+                const int tq = T1 - GS * q;
+                mb_wait(&S.empty[k][sl], ((seq / NS) & 1) ^ 1);
+                double *rg = &S.ring[k][sl][0][0][lane];
+#pragma unroll
+                for (int j = 0; j < GS; ++j) {
+                    const int tau = tq - j;
+                    unsigned im, bm;
+                    int o[8];
+                    tests(tau, im, bm, o);
+#pragma unroll
+                    for (int m = 0; m < 7; ++m)
+                        rg[(j * 8 + m) * 32] = ((im >> m) & 1u) ? (((bm >> m) & 1u) ? bl[j][m] : d[m][0]) : 0.0;
+                    rg[(j * 8 + 7) * 32] = ((bm >> 7) & 1u) ? bl[j][7] : d[7][0];
+                    if (tau >= lo && tau <= hi) {
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) march<K>(d[m]);
+                    }
+                    band_ld(tau - GS, bl[j]);
+                }
+                mb_arrive(&S.full[k][sl]);
             }
         }
         __syncthreads();
-        if (A.trace && threadIdx.x == 0) {
-            A.trace[TR * (int64_t)t + 1] = gtimer();
-            A.trace[TR * (int64_t)t + 2] = smid();
-            A.trace[TR * (int64_t)t + 3] = blockIdx.x;
-        }
+        trace_end(A, t);
     }
 }
 
@@ -848,6 +942,7 @@ struct Workspace {
     bool armed = false;
     cudaEvent_t done = nullptr;  // end of the last call that used this workspace
     long long *trace = nullptr;  // [2][ntasks][4] (TILU_PLANE_TRACE)
+    long long *steplog = nullptr;
     Maps maps;
 };
 
@@ -904,8 +999,8 @@ static bool launch_k(const PlanDev &P, const Args &A, const Maps &M, int ctas, b
 {
     static bool attrs = (set_attrs<K, EXACT, CONST_ROW>() == cudaSuccess);
     if (!attrs) return false;
-    if (fwd) k_plane_fwd<K, EXACT, CONST_ROW><<<ctas, PW * 32, sizeof(Smem), s>>>(P, A, M);
-    else k_plane_bwd<K, EXACT><<<ctas, PW * 32, sizeof(Smem), s>>>(P, A, M);
+    if (fwd) k_plane_fwd<K, EXACT, CONST_ROW><<<ctas, 3 * PW * 32, sizeof(Smem), s>>>(P, A, M);
+    else k_plane_bwd<K, EXACT><<<ctas, 2 * PW * 32, sizeof(Smem), s>>>(P, A, M);
     return true;
 }
 template <bool EXACT, bool CONST_ROW>
@@ -934,9 +1029,9 @@ static int resident_ctas(const tilu_plan *p)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     static const char *e = std::getenv("TILU_PLANE_CTAS_PER_SM");
-    int per = e ? std::atoi(e) : 2;
+    int per = e ? std::atoi(e) : 1;  // one CTA per SM (shared memory: ~166 KB per CTA)
     if (per < 1) per = 1;
-    if (per > 4) per = 4;
+    if (per > 1) per = 1;
     (void)p;
     return sms * per;
 }
@@ -949,6 +1044,8 @@ static int ws_create(tilu_plan *p, Workspace **out, cudaStream_t s)
     w->g = make_geo(p->dev.n);
     const size_t pe = (size_t)plane_elems(w->g);
     std::vector<int> tasks = make_tasks(p->dev.n);
+    static const char *nt = std::getenv("TILU_PLANE_NTASKS");  // debug: only the first N tasks (results invalid)
+    if (nt && std::atoi(nt) > 0 && (size_t)std::atoi(nt) < tasks.size()) tasks.resize(std::atoi(nt));
     w->ntasks = (int)tasks.size();
     w->ctas = std::min(w->ntasks, resident_ctas(p));
     void *m = nullptr;
@@ -969,8 +1066,8 @@ static int ws_create(tilu_plan *p, Workspace **out, cudaStream_t s)
     w->tasks = w->ticket + 8;
     cudaMemsetAsync(m, 0, bytes, s);
     cudaMemcpyAsync(w->tasks, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice, s);
-    if (!encode_map(&w->maps.u3, w->u, w->g, TG + 2, 3) || !encode_map(&w->maps.f1, w->f, w->g, TG, 1) ||
-        !encode_map(&w->maps.w1, w->W, w->g, TG, 1) || !encode_map(&w->maps.u1, w->u, w->g, TG, 1)) {
+    if (!encode_map(&w->maps.u3, w->u, w->g, GS + 4, 3) || !encode_map(&w->maps.f1, w->f, w->g, GS, 1) ||
+        !encode_map(&w->maps.w1, w->W, w->g, GS, 1) || !encode_map(&w->maps.u1, w->u, w->g, GS, 1)) {
         cudaFree(m);
         delete w;
         return TILU_ECUDA;
@@ -1038,9 +1135,16 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
     A.ntasks = w->ntasks;
     A.g = w->g;
     std::memcpy(A.arow, p->harow, sizeof(A.arow));
+    static const char *dbgv = std::getenv("TILU_PLANE_DBG");
+    A.dbg = dbgv ? std::atoi(dbgv) : 0;
     const bool exact = !(p->flags & TILU_FAST);
     static const char *trace_path = std::getenv("TILU_PLANE_TRACE");  // file: per-task timeline of the last sweep
     if (trace_path && !w->trace) cudaMalloc(&w->trace, 2 * (size_t)w->ntasks * TR * sizeof(long long));
+    static const char *steplog_path = std::getenv("TILU_PLANE_STEPLOG");
+    if (steplog_path && !w->steplog) {
+        cudaMalloc(&w->steplog, 3 * PW * 8 * sizeof(long long));
+        cudaMemset(w->steplog, 0, 3 * PW * 8 * sizeof(long long));
+    }
     prof_begin(s);
     k_plane_pack<<<P.nrows, 128, 0, s>>>(P, w->g, u, w->u);
     k_plane_pack<<<P.nrows, 128, 0, s>>>(P, w->g, f, w->f);
@@ -1056,12 +1160,14 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
         A.ticket = w->ticket;
         A.part = rnorm2 ? w->part : nullptr;
         A.trace = w->trace;
+        A.steplog = w->steplog;
         prof_begin(s);
         bool ok = launch_pass(P, A, w->maps, w->ctas, exact, true, s);
         prof_end("plane_fwd", s);
         A.ticket = w->ticket + 1;
         A.part = nullptr;
         A.trace = w->trace ? w->trace + (size_t)w->ntasks * TR : nullptr;
+        A.steplog = nullptr;
         static const char *dbg = std::getenv("TILU_PLANE_DEBUG");  // "1": forward pass only, return w_f
         if (dbg && dbg[0] == '1') {
             k_plane_unpack<<<P.nrows, 128, 0, s>>>(P, w->g, w->W, u);
@@ -1077,6 +1183,19 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
         if (rnorm2 && ok) {
             k_plane_norm<<<1, 1024, 0, s>>>(w->part, w->ntasks * PW * 32, rnorm2 + k);
             ++nl;
+        }
+    }
+    if (steplog_path && w->steplog) {
+        std::vector<long long> h(3 * PW * 8);
+        cudaMemcpy(h.data(), w->steplog, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+        if (FILE *fp = std::fopen(steplog_path, "w")) {
+            std::fprintf(fp, "warp total armed ringwait tmawait slowpath groups\n");
+            for (int wv = 0; wv < 3 * PW; ++wv) {
+                std::fprintf(fp, "%d", wv);
+                for (int i = 0; i < 6; ++i) std::fprintf(fp, " %lld", h[wv * 8 + i]);
+                std::fprintf(fp, "\n");
+            }
+            std::fclose(fp);
         }
     }
     if (trace_path && w->trace) {

@@ -1,0 +1,2 @@
+LEVEL=8 SWEEPS=1 SCHED=plane TILU_PLANE_NTASKS=1 TILU_PLANE_STEPLOG=gpurun_out/p13_steplog.txt timeout 300 python tools/plane_bench.py > gpurun_out/p13_bench.log 2>&1
+LEVEL=8 SWEEPS=1 SCHED=plane VARIANT=v2 TILU_PLANE_NTASKS=1 TILU_PLANE_STEPLOG=gpurun_out/p13_steplog_v2.txt timeout 300 python tools/plane_bench.py > gpurun_out/p13_bench_v2.log 2>&1

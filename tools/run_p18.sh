@@ -1,0 +1,3 @@
+LEVEL=8 SWEEPS=2 SCHED=plane TILU_PLANE_NTASKS=1 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_plane_fwd" -s 2 -c 1 -o gpurun_out/p18_full -f python tools/plane_bench.py > gpurun_out/p18_ncu.log 2>&1
+ncu -i gpurun_out/p18_full.ncu-rep --page source --csv --print-source sass > gpurun_out/p18_source.csv 2>/dev/null
+ncu -i gpurun_out/p18_full.ncu-rep --page raw --csv > gpurun_out/p18_raw.csv 2>/dev/null
