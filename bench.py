@@ -12,6 +12,10 @@ update) over every tet of the rank, inputs resident in HBM (u, f are 1.1 GB each
 than L2, so no flush is needed).  `e2e` = the same metric through the public API with
 pinned host buffers: H2D of u and f, `--e2e-sweeps` sweeps, D2H of u and the norms.
 
+The line also carries `single_tet` (rank 0, N=1): one macro-tet at level 9 (configs[2] geometry
+and size, k = 1) through the plane-layout band kernels -- the north star's single-tet target --
+with its own roofline fraction, API-call time and e2e from pinned host buffers.
+
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 """
@@ -270,6 +274,77 @@ def config_block(fit, world, extra=None) -> dict:
 # ----------------------------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------------------------
+def run_single(args) -> dict:
+    """One macro-tet at the north star's level (configs[2] geometry and size: unit tet, level 9,
+    q = 6 -> effective (4, 4, 4), V1, f ~ N(0, 1), u = 0) through the plane-layout band kernels.
+    The coefficient is k = 1 (constant stencil): config 3's variable k(x) needs the per-point
+    stencil assembled on the host (28 min in the reference) and a per-point residual; the sweep
+    kernels are the same.  Reported: device time per sweep of the two plane kernels (resident,
+    `value`), the API call time (pack + sweeps + unpack + norms per call), and e2e from pinned host
+    buffers (H2D u, f -> sweeps -> D2H u)."""
+    import torch
+
+    from paper_2210_15280_b200 import DevicePlan, _lib, fitting, lattice, stencil
+    level, q, sweeps = args.single_level, 6, args.single_sweeps
+    t0 = time.time()
+    src = stencil.stencil_source(lattice.unit_tet(), level, stencil.CoefficientField.constant(1.0))
+    fit = fitting.fit_surrogate_ilu(src, level, (q, q, q), "v1")
+    setup_s = time.time() - t0
+    N = lattice.interior_size(level)
+    mask = lattice.interior_mask(level)
+    f_host = np.zeros(lattice.grid_size(level))
+    f_host[mask] = np.random.default_rng(3).normal(size=int(mask.sum()))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data,
+                   fast=args.fast)
+    f = torch.as_tensor(f_host, device=dev)
+    u = torch.zeros_like(f)
+    p.sweep(u, f, 3)  # warm-up (workspace, arming, clocks)
+    torch.cuda.synchronize()
+    u.zero_()
+    _lib.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rn = p.sweep(u, f, sweeps, norms=True)
+    e1.record()
+    torch.cuda.synchronize()
+    kprof = _lib.profile_read()
+    _lib.profile_enable(False)
+    call_ms = e0.elapsed_time(e1) / sweeps
+    kern_ms = sum(tot for name, (cnt, tot) in kprof.items() if name in ("plane_fwd", "plane_bwd")) / sweeps
+    ab = algo_bytes(level, len(fit.band_ranks), "v1")["sweep"]
+    pk = peaks()
+    peak = pk.get("hbm_gbs") or HBM_FALLBACK
+    achieved = ab * N / (kern_ms / 1e3) / 1e9
+    # e2e: pinned host u, f -> device -> sweeps -> host u
+    uh = torch.zeros(f.numel(), dtype=torch.float64).pin_memory()
+    fh = torch.from_numpy(f_host).pin_memory()
+    torch.cuda.synchronize()
+    e0.record()
+    ud = uh.to(dev, non_blocking=True)
+    fd = fh.to(dev, non_blocking=True)
+    p.sweep(ud, fd, sweeps)
+    uh.copy_(ud, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    rho = float((rn[-1] / rn[-2]).sqrt()) if sweeps >= 2 else None
+    return {
+        "workload": f"configs[2] geometry/size with k=1: unit macro-tet, level {level} ({N} interior DoF), "
+                    f"q=6 eff {tuple(fit.degrees)}, V1, f~N(0,1) seed 3, u=0, {sweeps} sweeps per call",
+        "value": N / (kern_ms / 1e3), "unit": UNIT, "ms_per_sweep_kernels": kern_ms,
+        "ms_per_sweep_call": call_ms, "api_value": N / (call_ms / 1e3),
+        "roofline": {"bound": "hbm", "algorithmic_bytes_per_dof": ab, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak},
+        "e2e": {"value": N * sweeps / (e2e_ms / 1e3), "unit": UNIT, "ms": e2e_ms,
+                "h2d_bytes_per_step": 2 * f.numel() * 8, "d2h_bytes_per_step": f.numel() * 8,
+                "sweeps_per_step": sweeps, "api": "DevicePlan.sweep on device copies of pinned host u, f"},
+        "kernels": {k: {"launches": c, "avg_ms": t / c} for k, (c, t) in kprof.items()},
+        "residual_ratio_last": rho, "setup_s": setup_s,
+        "mode": "fast (FMA)" if args.fast else "exact (bitwise)",
+    }
+
+
 def run_ours(args, D: Dist):
     import torch
 
@@ -378,6 +453,13 @@ def run_ours(args, D: Dist):
         cpu = cpu_reference(fit, src, level, nt, threads)
         cpu.pop("seconds")
 
+    single = None
+    if D.world == 1 and D.rank == 0 and not args.no_single:
+        try:
+            single = run_single(args)
+        except Exception as e:  # reported, never silently replaced by another path
+            single = {"error": f"{type(e).__name__}: {e}"}
+
     if D.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D.world, "steps": args.steps,
@@ -390,6 +472,7 @@ def run_ours(args, D: Dist):
                                "peak": peak, "unit": "GB/s", "frac": sweep_achieved / peak},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "kernels": kernels, "clocks": clk,
             "residual_norm2_last": float(norms[-1][-1]) if norms else None,
+            "single_tet": single,
         }
         print(json.dumps(line), flush=True)
 
@@ -405,6 +488,9 @@ def main():
     ap.add_argument("--fast", action="store_true", help="FMA substitution (<=1e-12, not bitwise)")
     ap.add_argument("--simple", action="store_true", help="force the reference-layout kernels")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-single", action="store_true", help="skip the single-macro-tet (level 9) leg")
+    ap.add_argument("--single-level", type=int, default=9)
+    ap.add_argument("--single-sweeps", type=int, default=20)
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup raised to 3 (timing rules)")

@@ -31,7 +31,11 @@ for r in rows[2:]:
 json.dump(out, open(sys.argv[1], "w"), indent=1)
 traffic = {}
 for k, v in out.items():
-    fam = "batch_fwd" if "k_batch_fwd" in k else ("batch_bwd" if "k_batch_bwd" in k else None)
+    fam = None
+    for key, nm in (("k_batch_fwd", "batch_fwd"), ("k_batch_bwd", "batch_bwd"), ("k_plane_fwd", "plane_fwd"),
+                    ("k_plane_bwd", "plane_bwd")):
+        if key in k:
+            fam = nm
     if fam and v["dram_read_bytes"] is not None:
         traffic[fam] = v["dram_read_bytes"] + v["dram_write_bytes"]
 if len(sys.argv) > 2:
