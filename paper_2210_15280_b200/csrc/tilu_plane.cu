@@ -226,9 +226,9 @@ struct Smem {
 
 // Asynchronous 8-byte global -> shared copies (LDGSTS), tracked by commit groups instead of register
 // scoreboards, so a deep prefetch really stays in flight.
-__device__ __forceinline__ void cpa8(void *dst, const void *src)
+__device__ __forceinline__ void cpa8(uint32_t dst, const void *src)
 {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(dst)), "l"(src) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait_pd() { asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory"); }
@@ -414,16 +414,22 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                 // global handoff inputs of step tau, prefetched PD steps ahead into pre[k][tau & (PD-1)]
                 // (addresses of out-of-range steps stay inside the allocation and read boundary zeros)
                 double *pre = &S.pre[k][0][0][lane];
-                auto prefetch = [&](int tau) {
-                    double *d = pre + (tau & (PD - 1)) * 96;
-                    if (gp_on) cpa8(d, pw0 + tau * ZP);
+                const uint32_t pre_s = su32(pre);
+                // running source pointers of the prefetch stream (step tn = next step to prefetch)
+                const double *nw0 = pw0 + T0 * ZP, *nga = pga + T0 * ZP, *ngb = pgb + T0 * ZP;
+                int tn = T0;
+                auto prefetch = [&]() {
+                    const uint32_t d = pre_s + (uint32_t)((tn & (PD - 1)) * 96 * 8);
+                    if (gp_on) cpa8(d, nw0);
                     if (gl_on) {
-                        cpa8(d + 32, pga + tau * ZP);
-                        cpa8(d + 64, pgb + tau * ZP);
+                        cpa8(d + 32 * 8, nga);
+                        cpa8(d + 64 * 8, ngb);
                     }
                     cpa_commit();
+                    nw0 += ZP; nga += ZP; ngb += ZP; ++tn;
                 };
-                for (int i = 0; i < PD; ++i) prefetch(T0 + i);
+                for (int i = 0; i < PD; ++i) prefetch();
+                double *wo = pwo + T0 * ZP, *bo = pbo + T0 * ZP;  // own w_f / w_b handoff position at tau
                 double w1 = 0, w2 = 0, p1 = 0, p2 = 0, ga_prev = 0, gb_prev = 0;
                 const bool rearm_b = live && (k == 0 || (lane == 0 && z0 > 32));
                 auto grp = [&](const int q) {
@@ -489,13 +495,14 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                             if (p_on && k > 0) sts(hin + ((tau + 1) & (HR - 1)) * 32, sentv());
                             if (hout && tau >= T0 + 1) sts(hout + (tau & (HR - 1)) * 32, wnew);
                             if (vpt) {
-                                pwo[tau * ZP] = wnew;
-                                if (rearm_b) pbo[tau * ZP] = sentv();
+                                *wo = wnew;
+                                if (rearm_b) *bo = sentv();
                             }
+                            wo += ZP; bo += ZP;
                             ga_prev = ga_cur; gb_prev = gb_cur;
                             w2 = w1; w1 = wnew;
                             p2 = p1; p1 = p0;
-                            prefetch(tau + PD);
+                            prefetch();
                         }
                     }
                     mb_arrive(&S.empty[k][sl]);
@@ -709,16 +716,21 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                 double *pwo = A.W + pidx(g, s, 0, z);
                 const bool gp_on = (k == 0), gl_on = (lane == 31);
                 double *pre = &S.pre[k][0][0][lane];
-                auto prefetch = [&](int tau) {
-                    double *d = pre + (tau & (PD - 1)) * 96;
-                    if (gp_on) cpa8(d, pw0 + tau * ZP);
+                const uint32_t pre_s = su32(pre);
+                const double *nw0 = pw0 + T1 * ZP, *nga = pga + T1 * ZP, *ngb = pgb + T1 * ZP;
+                int tn = T1;
+                auto prefetch = [&]() {
+                    const uint32_t d = pre_s + (uint32_t)((tn & (PD - 1)) * 96 * 8);
+                    if (gp_on) cpa8(d, nw0);
                     if (gl_on) {
-                        cpa8(d + 32, pga + tau * ZP);
-                        cpa8(d + 64, pgb + tau * ZP);
+                        cpa8(d + 32 * 8, nga);
+                        cpa8(d + 64 * 8, ngb);
                     }
                     cpa_commit();
+                    nw0 -= ZP; nga -= ZP; ngb -= ZP; --tn;
                 };
-                for (int i = 0; i < PD; ++i) prefetch(T1 - i);
+                for (int i = 0; i < PD; ++i) prefetch();
+                double *uo = puo + T1 * ZP, *bo = pbo + T1 * ZP, *wo = pwo + T1 * ZP;
                 double wb1 = 0, wb2 = 0, q1 = 0, q2 = 0, ga_prev = 0, gb_prev = 0;
                 const bool b_out = live && (k == PW - 1 || (lane == 0 && z0 > 32));
                 const bool rearm_w = live && (k == 0 || lane == 31);
@@ -779,14 +791,15 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                             if (q_on && k > 0) sts(hin + ((tau - 1) & (HR - 1)) * 32, sentv());
                             if (hout && tau <= T1 - 1) sts(hout + (tau & (HR - 1)) * 32, wnew);
                             if (vpt) {
-                                puo[tau * ZP] = dadd(uv, acc);
-                                if (b_out) pbo[tau * ZP] = acc;
-                                if (rearm_w) pwo[tau * ZP] = sentv();
+                                *uo = dadd(uv, acc);
+                                if (b_out) *bo = acc;
+                                if (rearm_w) *wo = sentv();
                             }
+                            uo -= ZP; bo -= ZP; wo -= ZP;
                             ga_prev = ga_cur; gb_prev = gb_cur;
                             wb2 = wb1; wb1 = wnew;
                             q2 = q1; q1 = q0;
-                            prefetch(tau - PD);
+                            prefetch();
                         }
                     }
                     __syncwarp();
