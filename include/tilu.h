@@ -146,6 +146,12 @@ void tilu_profile_enable(int on);
 void tilu_profile_reset(void);
 int tilu_profile_read(char *names /* cap * 64 bytes */, int *counts, double *ms, int cap);
 
+/* Band tasks of the single-tet plane kernels at a level (n = 2^level): codes (b << 16) | c for band b
+ * (diagonals s = 2 + 4b .. 5 + 4b) and 32-row chunk c (rows z = 1 + 32c .. 32 + 32c), in the forward
+ * pass's topological order (the backward pass takes them reversed).  Writes up to cap codes and
+ * returns the task count (introspection and tests; no device work). */
+int tilu_plane_tasks(int level, int *out, int cap);
+
 /* Plan geometry: grid size and interior DoF count. */
 int64_t tilu_plan_grid_size(const tilu_plan_t *plan);
 int64_t tilu_plan_interior_size(const tilu_plan_t *plan);

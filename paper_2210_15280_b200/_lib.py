@@ -47,7 +47,7 @@ EXPORTS = (
     "tilu_version", "tilu_last_launch_count", "tilu_plan_grid_size", "tilu_plan_interior_size",
     "tilu_profile_enable", "tilu_profile_reset", "tilu_profile_read", "tilu_packed_size",
     "tilu_packed_scratch_size", "tilu_pack",
-    "tilu_unpack", "tilu_sweep_packed",
+    "tilu_unpack", "tilu_sweep_packed", "tilu_plane_tasks",
 )
 
 
@@ -91,6 +91,8 @@ def lib():
         getattr(L, name).restype = _I
     L.tilu_sweep_packed.argtypes = [_P, _P, _P, _P, _I, _I, _P, _P]
     L.tilu_sweep_packed.restype = _I
+    L.tilu_plane_tasks.argtypes = [_I, _P, _I]
+    L.tilu_plane_tasks.restype = _I
     L.tilu_profile_enable.argtypes = [_I]
     L.tilu_profile_enable.restype = None
     L.tilu_profile_reset.restype = None
@@ -126,3 +128,12 @@ def profile_read() -> dict:
         nm = names.raw[64 * i:64 * (i + 1)].split(b"\0", 1)[0].decode()
         out[nm] = (int(counts[i]), float(ms[i]))
     return out
+
+
+def plane_tasks(level: int) -> list[tuple[int, int]]:
+    """(band, chunk) tasks of the single-tet plane kernels in forward topological order."""
+    L = lib()
+    n = int(L.tilu_plane_tasks(int(level), None, 0))
+    buf = (ctypes.c_int * max(n, 1))()
+    L.tilu_plane_tasks(int(level), buf, n)
+    return [(v >> 16, v & 0xFFFF) for v in buf[:n]]

@@ -1096,6 +1096,14 @@ static int ws_create(tilu_plan *p, Workspace **out, cudaStream_t s)
 
 }  // namespace pl
 
+extern "C" int tilu_plane_tasks(int level, int *out, int cap)
+{
+    if (level < 2 || level > 12) return -1;
+    const std::vector<int> t = pl::make_tasks(1 << level);
+    for (int i = 0; i < (int)t.size() && i < cap && out; ++i) out[i] = t[i];
+    return (int)t.size();
+}
+
 bool plane_supported(const tilu_plan *p)
 {
     if (p->flags & TILU_SCHED_SIMPLE) return false;
