@@ -62,7 +62,10 @@ constexpr int GS = 4;    // steps per group: helper ring and TMA unit, unroll fa
 constexpr int NS = 2;    // helper -> solver ring depth (groups)
 constexpr int NT = 3;    // TMA ring depth (groups)
 constexpr int HR = 8;    // solver -> solver handoff ring depth (steps), power of two
-constexpr int PD = 8;    // global handoff prefetch distance (steps), power of two
+#ifndef TILU_PLANE_PD
+#define TILU_PLANE_PD 2
+#endif
+constexpr int PD = TILU_PLANE_PD;  // global handoff prefetch distance (steps), power of two
 constexpr int WIN = 34;  // doubles per staged line: z0-1 .. z0+32
 // one staged group: forward u box [3 planes s-1..s+1][GS+4 lines][WIN] + f box [GS][WIN];
 // backward w_f box [GS][WIN] + u box [GS][WIN]  (tensor copies need 128-byte aligned destinations)
