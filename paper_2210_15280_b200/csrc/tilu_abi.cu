@@ -42,7 +42,7 @@ void prof_end(const char *name, cudaStream_t s);
 bool plane_supported(const tilu_plan *plan);
 void plane_free(void *ws);
 int plane_sweep(const tilu_plan *plan, double *u, const double *f, int ntets, int sweeps, double *rnorm2,
-                cudaStream_t s, int *launches);
+                cudaStream_t s, int *launches, bool stored);
 }  // namespace tilu
 
 using namespace tilu;
@@ -574,10 +574,10 @@ static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int nt
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const PlanDev &P = p->dev;
     // One macro-tet: the plane-layout band kernels (tilu_plane.cu) parallelise the sweep inside the tet.
-    if (!stored && ntets == 1 && plane_supported(p) && !(p->flags & TILU_SCHED_BATCH) &&
+    if (ntets == 1 && plane_supported(p) && !(p->flags & TILU_SCHED_BATCH) &&
         ((p->flags & TILU_SCHED_PLANE) || P.level >= plane_min_level())) {
         int nl = 0;
-        const int rc = plane_sweep(p, u, f, ntets, sweeps, rnorm2, s, &nl);
+        const int rc = plane_sweep(p, u, f, ntets, sweeps, rnorm2, s, &nl, stored);
         g_launches += nl;
         if (rc) return fail(rc, "plane sweep failed (%d): %s", rc, cudaGetErrorString(cudaGetLastError()));
         return check_cuda("plane sweep");

@@ -107,6 +107,7 @@ struct Args {
     long long *steplog;    // TILU_PLANE_STEPLOG: [PW][2048] clock64 at every step of task 0 (or nullptr)
     long long *trace;      // TILU_PLANE_TRACE: [ntasks][4] = start ns, end ns, sm id, CTA (or nullptr)
     Geo g;
+    int stored;            // 1: L / 1/D from the stored ILU(0) factors (CellILU, ilu.py:210-227) instead of NDDF
     int dbg;               // TILU_PLANE_DBG bits (timing experiments only, results invalid): 1 = no global handoff loads
     double arow[15];       // constant stencil (kernel-parameter bank)
 };
@@ -518,6 +519,7 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
             // ============================ march helper ==========================================
             double d[7][K];
             int boff = 0;
+            int64_t rbase = 0;
             if (live) {
                 const int r = row_id(n, z, y);
                 const double *sd = P.seedF + (int64_t)r * 7 * K;
@@ -526,19 +528,23 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
 #pragma unroll
                     for (int j = 0; j < K; ++j) d[m][j] = sd[m * K + j];
                 if (P.variant == 1) boff = P.bandoff[r];
+                rbase = P.rowbase[r];
             } else {
 #pragma unroll
                 for (int m = 0; m < 7; ++m)
 #pragma unroll
                     for (int j = 0; j < K; ++j) d[m][j] = 0.0;
             }
-            const bool v1 = P.variant == 1;
+            const bool v1 = P.variant == 1, stored = A.stored != 0;
             const bool rowband = z == 1 || y == 1;
-            // V1 band rows, loaded GS steps ahead: bl[j] = store row of step tq + j (when a band point)
+            // Loaded GS steps ahead: bl[j] = V1 band row of step tq + j (when a band point), or with
+            // stored factors the factor row of every point (_kernels.py:150-166 reads factors[p, m])
             auto band_ld = [&](int tau, double(&v)[7]) {
-                const bool isb = v1 && tau >= lo && tau <= hi && (rowband || tau == lo || tau == hi);
+                const bool vp = tau >= lo && tau <= hi;
                 const int x = tau - z;
-                const double *st = P.store + 9 * (int64_t)(boff + (rowband ? x - 1 : (tau == lo ? 0 : 1)));
+                const bool isb = stored ? vp : (v1 && vp && (rowband || tau == lo || tau == hi));
+                const double *st = stored ? P.factors + 9 * (rbase + x)
+                                          : P.store + 9 * (int64_t)(boff + (rowband ? x - 1 : (tau == lo ? 0 : 1)));
 #pragma unroll
                 for (int m = 0; m < 7; ++m) v[m] = ld_if(isb, st + m, 0.0);
             };
@@ -558,10 +564,10 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                 for (int j = 0; j < GS; ++j) {
                     const int tau = tq + j;
                     const bool vpt = tau >= lo && tau <= hi;
-                    const bool isb = v1 && vpt && (rowband || tau == lo || tau == hi);
+                    const bool isb = stored || (v1 && vpt && (rowband || tau == lo || tau == hi));
 #pragma unroll
                     for (int m = 0; m < 7; ++m) rg[(j * 8 + m) * 32] = isb ? bl[j][m] : d[m][0];
-                    if (vpt) {
+                    if (vpt && !stored) {
 #pragma unroll
                         for (int m = 0; m < 7; ++m) march<K>(d[m]);
                     }
@@ -818,6 +824,7 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
             // ============================ march helper ==========================================
             double d[8][K];
             int bo_own = 0, bo_n = 0, bo_ts = 0, bo_tc = 0;
+            int64_t rb_own = 0, rb_n = 0, rb_ts = 0, rb_tc = 0;  // row bases (stored factors)
             if (live) {
                 const int r = row_id(n, z, y);
                 const double *sd = P.seedB + (int64_t)r * 8 * K;
@@ -825,6 +832,12 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                 for (int m = 0; m < 8; ++m)
 #pragma unroll
                     for (int j = 0; j < K; ++j) d[m][j] = sd[m * K + j];
+                rb_own = P.rowbase[r];
+                if (s + 1 <= n - 2) {
+                    rb_n = P.rowbase[row_id(n, z, y + 1)];
+                    rb_tc = P.rowbase[row_id(n, z + 1, y)];
+                }
+                if (y >= 2) rb_ts = P.rowbase[row_id(n, z + 1, y - 1)];
                 if (P.variant == 1) {
                     bo_own = P.bandoff[r];
                     if (s + 1 <= n - 2) {
@@ -839,7 +852,7 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
 #pragma unroll
                     for (int j = 0; j < K; ++j) d[m][j] = 0.0;
             }
-            const bool v1 = P.variant == 1;
+            const bool v1 = P.variant == 1, stored = A.stored != 0;
             const bool zr1 = z == 1, yr1 = y == 1, yr2 = y == 2, yge2 = y >= 2;
             // band / interior tests of the seven source points q_m = p - d_m (_lq, _kernels.py:434-441)
             // and of p (1/D).  Masks: bit m = q_m interior (m < 7); band bits in bmask (bit 7 = p).
@@ -870,6 +883,16 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                 unsigned im, bm;
                 int o[8];
                 tests(tau, im, bm, o);
+                if (stored) {  // factors of the source points q_m (transposed entries) and 1/D at p (_kernels.py:169-192)
+                    const int x = tau - z;
+                    const bool vp = tau >= lo && tau <= hi;
+                    const int64_t rk[8] = {rb_own + x + 1, rb_n + x, rb_n + x - 1, rb_ts + x + 1,
+                                           rb_ts + x,      rb_tc + x, rb_tc + x - 1, rb_own + x};
+#pragma unroll
+                    for (int m = 0; m < 8; ++m)
+                        v[m] = ld_if(vp && (m == 7 || ((im >> m) & 1u)), P.factors + 9 * rk[m] + (m < 7 ? m : 8), 0.0);
+                    return;
+                }
 #pragma unroll
                 for (int m = 0; m < 8; ++m) v[m] = ld_if((bm >> m) & 1u, P.store + 9 * (int64_t)o[m] + (m < 7 ? m : 8), 0.0);
             };
@@ -887,11 +910,12 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                     unsigned im, bm;
                     int o[8];
                     tests(tau, im, bm, o);
+                    if (stored) bm = 0xFFu;
 #pragma unroll
                     for (int m = 0; m < 7; ++m)
                         rg[(j * 8 + m) * 32] = ((im >> m) & 1u) ? (((bm >> m) & 1u) ? bl[j][m] : d[m][0]) : 0.0;
                     rg[(j * 8 + 7) * 32] = ((bm >> 7) & 1u) ? bl[j][7] : d[7][0];
-                    if (tau >= lo && tau <= hi) {
+                    if (tau >= lo && tau <= hi && !stored) {
 #pragma unroll
                         for (int m = 0; m < 8; ++m) march<K>(d[m]);
                     }
@@ -1130,7 +1154,7 @@ int64_t plane_interior_points(const tilu_plan *p) { return p->interior; }
 
 // `sweeps` smoothing steps on one macro-tet in the reference layout: pack, sweeps, unpack.
 int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int sweeps, double *rnorm2,
-                cudaStream_t s, int *launches)
+                cudaStream_t s, int *launches, bool stored)
 {
     using namespace pl;
     tilu_plan *p = const_cast<tilu_plan *>(cp);
@@ -1161,6 +1185,8 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
     std::memcpy(A.arow, p->harow, sizeof(A.arow));
     static const char *dbgv = std::getenv("TILU_PLANE_DBG");
     A.dbg = dbgv ? std::atoi(dbgv) : 0;
+    A.stored = stored ? 1 : 0;
+    if (stored && !p->dev.factors) return TILU_EINVAL;
     const bool exact = !(p->flags & TILU_FAST);
     static const char *trace_path = std::getenv("TILU_PLANE_TRACE");  // file: per-task timeline of the last sweep
     if (trace_path && !w->trace) cudaMalloc(&w->trace, 2 * (size_t)w->ntasks * TR * sizeof(long long));

@@ -115,3 +115,18 @@ def test_plane_boundary_untouched():
     u = cuda(u0b)
     plane_plan(level, src, fit, "v1").sweep(u, cuda(f), 2)
     assert np.all(u.cpu().numpy()[~mask] == 0.0)
+
+
+@pytest.mark.parametrize("level", [5, 7])
+def test_plane_stored_factor_sweep_bitwise(level):
+    """CellILU (stored ILU(0) factors, ilu.py:210-227) through the plane kernels: the march helpers
+    read the factor rows instead of marching surrogates."""
+    src, fit, u0, f = case(level, 4, fseed=11)
+    fr = F.factorize_tet(src, level, full_store=True)
+    ref = u0.copy()
+    O.sweeps(None, level, src.data, ref, f, 3, factors=fr.rows)
+    p = DevicePlan(level, np.zeros((7, 1, 1, 1)), np.zeros(1), "v2", factors=fr.rows, arow=src.data,
+                   schedule="plane")
+    u = cuda(u0)
+    p.sweep(u, cuda(f), 3, stored=True)
+    assert np.array_equal(u.cpu().numpy(), ref)
