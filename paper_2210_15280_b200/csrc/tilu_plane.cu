@@ -545,8 +545,10 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                 const bool isb = stored ? vp : (v1 && vp && (rowband || tau == lo || tau == hi));
                 const double *st = stored ? P.factors + 9 * (rbase + x)
                                           : P.store + 9 * (int64_t)(boff + (rowband ? x - 1 : (tau == lo ? 0 : 1)));
+                if (__any_sync(0xffffffffu, isb)) {
 #pragma unroll
-                for (int m = 0; m < 7; ++m) v[m] = ld_if(isb, st + m, 0.0);
+                    for (int m = 0; m < 7; ++m) v[m] = ld_if(isb, st + m, 0.0);
+                }
             };
             double bl[GS][7];
 #pragma unroll
@@ -879,13 +881,14 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                 o[6] = bo_tc + (yr1 ? x - 2 : (x2 ? 0 : 1));
                 o[7] = bo_own + ((zr1 || yr1) ? x - 1 : (x1 ? 0 : 1));
             };
-            auto band_ld = [&](int tau, double(&v)[8]) {
-                unsigned im, bm;
+            // masks and band / factor values of step tau, computed GS steps ahead (one tests() per step)
+            auto band_ld = [&](int tau, double(&v)[8], unsigned &im, unsigned &bm) {
                 int o[8];
                 tests(tau, im, bm, o);
                 if (stored) {  // factors of the source points q_m (transposed entries) and 1/D at p (_kernels.py:169-192)
                     const int x = tau - z;
                     const bool vp = tau >= lo && tau <= hi;
+                    bm = vp ? 0xFFu : 0u;
                     const int64_t rk[8] = {rb_own + x + 1, rb_n + x, rb_n + x - 1, rb_ts + x + 1,
                                            rb_ts + x,      rb_tc + x, rb_tc + x - 1, rb_own + x};
 #pragma unroll
@@ -893,12 +896,16 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                         v[m] = ld_if(vp && (m == 7 || ((im >> m) & 1u)), P.factors + 9 * rk[m] + (m < 7 ? m : 8), 0.0);
                     return;
                 }
+                if (__any_sync(0xffffffffu, bm != 0u)) {
 #pragma unroll
-                for (int m = 0; m < 8; ++m) v[m] = ld_if((bm >> m) & 1u, P.store + 9 * (int64_t)o[m] + (m < 7 ? m : 8), 0.0);
+                    for (int m = 0; m < 8; ++m)
+                        v[m] = ld_if((bm >> m) & 1u, P.store + 9 * (int64_t)o[m] + (m < 7 ? m : 8), 0.0);
+                }
             };
             double bl[GS][8];
+            unsigned bim[GS], bbm[GS];
 #pragma unroll
-            for (int j = 0; j < GS; ++j) band_ld(T1 - j, bl[j]);
+            for (int j = 0; j < GS; ++j) band_ld(T1 - j, bl[j], bim[j], bbm[j]);
             for (int q = 0; q < ngroups; ++q, ++seq) {
                 const int sl = seq % NS;
                 const int tq = T1 - GS * q;
@@ -907,10 +914,7 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
 #pragma unroll
                 for (int j = 0; j < GS; ++j) {
                     const int tau = tq - j;
-                    unsigned im, bm;
-                    int o[8];
-                    tests(tau, im, bm, o);
-                    if (stored) bm = 0xFFu;
+                    const unsigned im = bim[j], bm = bbm[j];
 #pragma unroll
                     for (int m = 0; m < 7; ++m)
                         rg[(j * 8 + m) * 32] = ((im >> m) & 1u) ? (((bm >> m) & 1u) ? bl[j][m] : d[m][0]) : 0.0;
@@ -919,7 +923,7 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
 #pragma unroll
                         for (int m = 0; m < 8; ++m) march<K>(d[m]);
                     }
-                    band_ld(tau - GS, bl[j]);
+                    band_ld(tau - GS, bl[j], bim[j], bbm[j]);
                 }
                 mb_arrive(&S.full[k][sl]);
             }
@@ -1006,18 +1010,28 @@ static bool encode_map(CUtensorMap *m, double *base, const Geo &g, int box_tau, 
            CUDA_SUCCESS;
 }
 
-// Band tasks in topological order: key 18 b + 32 c (a band starts ~18 steps after the one below it,
-// a chunk 32 steps after the one below it); every dependency ((b-1, c), (b-1, c-1), (b, c-1)) has a
-// strictly smaller key.
+// Band tasks in topological order: key kb b + kc c; every dependency ((b-1, c), (b-1, c-1), (b, c-1))
+// has a strictly smaller key.
 static std::vector<int> make_tasks(int n)
 {
+    // start-time model: a band starts ~7 steps after the band below (4 diagonals x 2-step lag + the
+    // global hop), a chunk ~36 steps after the chunk below (32-lane skew + hop); TILU_PLANE_KEY=kb,kc
+    // overrides (measurement only).  Any positive weights keep the order topological.
+    long long kb = 7, kc = 36;
+    if (const char *e = std::getenv("TILU_PLANE_KEY")) {
+        long long a = 0, c = 0;
+        if (std::sscanf(e, "%lld,%lld", &a, &c) == 2 && a > 0 && c > 0) {
+            kb = a;
+            kc = c;
+        }
+    }
     std::vector<std::pair<long long, int>> v;
     for (int b = 0;; ++b) {
         const int s0 = 2 + PW * b;
         if (s0 > n - 2) break;
         const int smax = std::min(s0 + PW - 1, n - 2);
         const int nch = (smax - 1 + 31) / 32;
-        for (int c = 0; c < nch; ++c) v.push_back({(18ll * b + 32ll * c) * 65536 + c, (b << 16) | c});
+        for (int c = 0; c < nch; ++c) v.push_back({(kb * b + kc * c) * 65536 + c, (b << 16) | c});
     }
     std::sort(v.begin(), v.end());
     std::vector<int> out;
