@@ -490,7 +490,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-single", action="store_true", help="skip the single-macro-tet (level 9) leg")
     ap.add_argument("--single-level", type=int, default=9)
-    ap.add_argument("--single-sweeps", type=int, default=20)
+    ap.add_argument("--single-sweeps", type=int, default=100)
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup raised to 3 (timing rules)")

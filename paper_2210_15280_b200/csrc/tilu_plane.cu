@@ -108,7 +108,6 @@ struct Args {
     long long *trace;      // TILU_PLANE_TRACE: [ntasks][4] = start ns, end ns, sm id, CTA (or nullptr)
     Geo g;
     int stored;            // 1: L / 1/D from the stored ILU(0) factors (CellILU, ilu.py:210-227) instead of NDDF
-    int dbg;               // TILU_PLANE_DBG bits (timing experiments only, results invalid): 1 = no global handoff loads
     double arow[15];       // constant stencil (kernel-parameter bank)
 };
 
@@ -135,13 +134,6 @@ __device__ __forceinline__ void mb_wait(uint64_t *b, uint32_t parity)
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void bulk(void *dst, const void *src, uint32_t bytes, uint64_t *b)
-{
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     su32(dst)),
-                 "l"(src), "r"(bytes), "r"(su32(b))
-                 : "memory");
-}
 __device__ __forceinline__ void tma3(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *b)
 {
     asm volatile(
@@ -157,16 +149,6 @@ __device__ __forceinline__ bool is_sent(double v) { return __double_as_longlong(
 __device__ __forceinline__ double lds_vol(const double *p) { return *reinterpret_cast<const volatile double *>(p); }
 __device__ __forceinline__ void sts(double *p, double v) { *reinterpret_cast<volatile double *>(p) = v; }
 __device__ __forceinline__ double ldg_cg(const double *p) { return __ldcg(p); }
-// Speculative prefetch of a handoff value: a weak (L1-cacheable, pipelined) load.  Safe because a
-// handoff position only ever changes once per pass (sentinel -> final value) and L1 starts every
-// kernel empty: a stale copy can only be the sentinel, which sends the consumer to the strong
-// polling path (ldg_cg).
-__device__ __forceinline__ double ldg_pf(const double *p)
-{
-    double v;
-    asm("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));  // weak, not volatile: may be scheduled freely
-    return v;
-}
 __device__ __forceinline__ long long gtimer()
 {
     long long t;
@@ -180,17 +162,6 @@ __device__ __forceinline__ int smid()
     return v;
 }
 
-// Warp-uniform wait until no lane holds the sentinel (global value re-read from L2).  A dependency
-// bug must fail loudly instead of hanging the device: trap after ~2^26 re-reads.
-__device__ __forceinline__ void ready_g(double &v, const double *p, bool mine)
-{
-    long long spins = 0;
-    while (__any_sync(0xffffffffu, mine && is_sent(v))) {
-        __nanosleep(40);
-        if (mine) v = ldg_cg(p);
-        if (++spins > (1ll << 26)) __trap();
-    }
-}
 // Shared-memory handoff: take the value of slot p (wait until produced), re-arm the slot.
 __device__ __forceinline__ double take_s(double *p)
 {
@@ -936,21 +907,53 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
 // ------------------------------------------------------------------------------------------------
 // Layout conversion, arming, norms.
 // ------------------------------------------------------------------------------------------------
-// One CTA per interior row (z, y); threads over x.
-__global__ void k_plane_pack(const PlanDev P, Geo g, const double *__restrict__ src, double *__restrict__ dst)
+// Layout conversion by 32 x 32 tiles of one diagonal plane s: (tau block, z block).  A warp reads
+// whole segments of 32 consecutive x of one reference row (coalesced), the tile is transposed in
+// shared memory, and every plane line (fixed tau, 32 consecutive z) is written as one segment.
+// grid = (tau blocks, z blocks, diagonals 2 .. n-2); UNPACK reverses the direction.
+template <bool UNPACK>
+__global__ void __launch_bounds__(256) k_plane_xpose(const PlanDev P, Geo g, const double *__restrict__ src,
+                                                     double *__restrict__ dst)
 {
-    const RowInfo ri = P.rows[blockIdx.x];
-    const int64_t base = P.rowbase[blockIdx.x];
-    const int s = ri.y + ri.z;
-    for (int x = 1 + threadIdx.x; x <= ri.xe; x += blockDim.x) dst[pidx(g, s, x + ri.z, ri.z)] = src[base + x];
+    __shared__ double tile[32][33];
+    const int n = P.n;
+    const int s = 2 + blockIdx.z, tau0 = 2 + 32 * blockIdx.x, z0 = 1 + 32 * blockIdx.y;
+    const int xe = n - 1 - s;
+    if (z0 > s - 1 || tau0 > z0 + 31 + xe || tau0 + 31 < z0 + 1) return;  // no interior point in the tile
+    const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+    if (!UNPACK) {
+        // reference rows z = z0 + r: x = tau - z for tau = tau0 + lane
+        for (int r = wy; r < 32; r += 8) {
+            const int z = z0 + r, x = tau0 + lane - z;
+            double v = 0.0;
+            if (z <= s - 1 && x >= 1 && x <= xe) v = src[row_offset(n, z, s - z) + x];
+            tile[r][lane] = v;
+        }
+        __syncthreads();
+        for (int c = wy; c < 32; c += 8) {  // plane line tau = tau0 + c, z = z0 + lane
+            const int z = z0 + lane, x = tau0 + c - z;
+            if (z <= s - 1 && x >= 1 && x <= xe) dst[pidx(g, s, tau0 + c, z)] = tile[lane][c];
+        }
+    } else {
+        for (int c = wy; c < 32; c += 8) {
+            const int z = z0 + lane, x = tau0 + c - z;
+            tile[lane][c] = (z <= s - 1 && x >= 1 && x <= xe) ? src[pidx(g, s, tau0 + c, z)] : 0.0;
+        }
+        __syncthreads();
+        for (int r = wy; r < 32; r += 8) {
+            const int z = z0 + r, x = tau0 + lane - z;
+            if (z <= s - 1 && x >= 1 && x <= xe) dst[row_offset(n, z, s - z) + x] = tile[r][lane];
+        }
+    }
 }
-__global__ void k_plane_unpack(const PlanDev P, Geo g, const double *__restrict__ src, double *__restrict__ dst)
+static void launch_xpose(const PlanDev &P, const Geo &g, const double *src, double *dst, bool unpack, cudaStream_t s)
 {
-    const RowInfo ri = P.rows[blockIdx.x];
-    const int64_t base = P.rowbase[blockIdx.x];
-    const int s = ri.y + ri.z;
-    for (int x = 1 + threadIdx.x; x <= ri.xe; x += blockDim.x) dst[base + x] = src[pidx(g, s, x + ri.z, ri.z)];
+    const int n = P.n;
+    const dim3 grid((n - 3 + 31) / 32, (n - 3 + 31) / 32, n - 3);
+    if (unpack) k_plane_xpose<true><<<grid, 256, 0, s>>>(P, g, src, dst);
+    else k_plane_xpose<false><<<grid, 256, 0, s>>>(P, g, src, dst);
 }
+
 // Arm the forward handoff positions of W: last diagonal of every band, rows z = 0 mod 32.
 __global__ void k_plane_arm(const PlanDev P, Geo g, double *__restrict__ W)
 {
@@ -1197,8 +1200,6 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
     A.ntasks = w->ntasks;
     A.g = w->g;
     std::memcpy(A.arow, p->harow, sizeof(A.arow));
-    static const char *dbgv = std::getenv("TILU_PLANE_DBG");
-    A.dbg = dbgv ? std::atoi(dbgv) : 0;
     A.stored = stored ? 1 : 0;
     if (stored && !p->dev.factors) return TILU_EINVAL;
     const bool exact = !(p->flags & TILU_FAST);
@@ -1210,8 +1211,8 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
         cudaMemset(w->steplog, 0, 3 * PW * 8 * sizeof(long long));
     }
     prof_begin(s);
-    k_plane_pack<<<P.nrows, 128, 0, s>>>(P, w->g, u, w->u);
-    k_plane_pack<<<P.nrows, 128, 0, s>>>(P, w->g, f, w->f);
+    launch_xpose(P, w->g, u, w->u, false, s);
+    launch_xpose(P, w->g, f, w->f, false, s);
     if (!w->armed) {
         k_plane_arm<<<P.nrows, 128, 0, s>>>(P, w->g, w->W);
         ++nl;
@@ -1234,7 +1235,7 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
         A.steplog = nullptr;
         static const char *dbg = std::getenv("TILU_PLANE_DEBUG");  // "1": forward pass only, return w_f
         if (dbg && dbg[0] == '1') {
-            k_plane_unpack<<<P.nrows, 128, 0, s>>>(P, w->g, w->W, u);
+            launch_xpose(P, w->g, w->W, u, true, s);
             w->armed = false;
             cudaEventRecord(w->done, s);
             return ok ? TILU_OK : TILU_EUNSUPPORTED;
@@ -1282,7 +1283,7 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
         }
     }
     prof_begin(s);
-    k_plane_unpack<<<P.nrows, 128, 0, s>>>(P, w->g, w->u, u);
+    launch_xpose(P, w->g, w->u, u, true, s);
     prof_end("plane_unpack", s);
     ++nl;
     if (cudaGetLastError() != cudaSuccess) {
