@@ -302,15 +302,13 @@ __device__ __forceinline__ void trace_end(const Args &A, int t)
 // a group of GS steps, the GS ring slots it will write must be armed (consumed).
 __device__ __forceinline__ void wait_armed(const double *hout, int t_first, int dir, int lo, int hi)
 {
+    // The consumer re-arms the slots in step order, so the slot of the group's last step being armed
+    // implies all of them are.
+    const int tl = dir > 0 ? min(t_first + GS - 1, hi) : max(t_first - (GS - 1), lo);
+    if (tl < lo || tl > hi) return;
+    const double *p = hout + (tl & (HR - 1)) * 32;
     long long spins = 0;
-    for (;;) {
-        bool busy = false;
-#pragma unroll
-        for (int k = 0; k < GS; ++k) {
-            const int tt = t_first + dir * k;
-            if (tt >= lo && tt <= hi) busy |= !is_sent(lds_vol(hout + (tt & (HR - 1)) * 32));
-        }
-        if (!__any_sync(0xffffffffu, busy)) break;
+    while (__any_sync(0xffffffffu, !is_sent(lds_vol(p)))) {
         if (++spins > (1ll << 28)) __trap();
     }
 }

@@ -130,3 +130,17 @@ def test_plane_stored_factor_sweep_bitwise(level):
     u = cuda(u0)
     p.sweep(u, cuda(f), 3, stored=True)
     assert np.array_equal(u.cpu().numpy(), ref)
+
+
+def test_plane_config3_variable_coefficient():
+    """Config 3's coefficient k(x) = 1 + 0.5 sin(2 pi x) sin(2 pi y) sin(2 pi z) (per-point stencil
+    rows, f ~ N(0, 1), u = 0) through the plane kernels, bitwise vs the oracle."""
+    level = 6
+    src, fit, _, f = case(level, 6, "v1", coeff=S.sin_kappa(), fseed=3)
+    assert not src.constant
+    u0 = np.zeros_like(f)
+    ref, nr = oracle_sweeps(level, src, fit, "v1", u0, f, 3)
+    u = cuda(u0)
+    rn = plane_plan(level, src, fit, "v1").sweep(u, cuda(f), 3, norms=True)
+    assert np.array_equal(u.cpu().numpy(), ref)
+    np.testing.assert_allclose(rn.cpu().numpy().ravel(), nr, rtol=1e-12)
