@@ -429,22 +429,9 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                             const double *pv = pre + (tau & (PD - 1)) * 96;
                             if (p_on) p0 = gp_on ? pv[0] : lds_vol(hin + ((tau + 1) & (HR - 1)) * 32);
                             double ga_cur = pv[32], gb_cur = pv[64];
-                            double lw1 = __shfl_up_sync(0xffffffffu, w1, 1);
-                            double lw2 = __shfl_up_sync(0xffffffffu, w2, 1);
-                            double lp1 = __shfl_up_sync(0xffffffffu, p1, 1);
-                            double lp2 = __shfl_up_sync(0xffffffffu, p2, 1);
-                            lw1 = gl_on ? ga_cur : lw1;
-                            lw2 = gl_on ? ga_prev : lw2;
-                            lp1 = gl_on ? gb_cur : lp1;
-                            lp2 = gl_on ? gb_prev : lp2;
-                            double L[7];
-#pragma unroll
-                            for (int m = 0; m < 7; ++m) L[m] = rg[(j * 8 + m) * 32];
-                            const double r = rg[(j * 8 + 7) * 32];
-                            double acc = fwd_chain<EXACT>(r, L, w1, p1, p0, lw2, lw1, lp2, lp1);
-                            const bool bad = p_on && (is_sent(p0) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur))));
-                            if (__any_sync(0xffffffffu, bad)) {
-                                PLN_T0();
+                            // acquire: inputs produced by other warps must be final before the chain runs
+                            if (__any_sync(0xffffffffu,
+                                           p_on && (is_sent(p0) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur)))))) {
                                 long long spins = 0;
                                 for (;;) {
                                     if (p_on && is_sent(p0)) p0 = gp_on ? ldg_cg(pw0 + tau * ZP)
@@ -458,11 +445,20 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                                     if (!__any_sync(0xffffffffu, still)) break;
                                     if (++spins > (1ll << 26)) __trap();
                                 }
-                                lw1 = gl_on ? ga_cur : lw1;
-                                lp1 = gl_on ? gb_cur : lp1;
-                                acc = fwd_chain<EXACT>(r, L, w1, p1, p0, lw2, lw1, lp2, lp1);
-                                PLN_ADD(4);
                             }
+                            double lw1 = __shfl_up_sync(0xffffffffu, w1, 1);
+                            double lw2 = __shfl_up_sync(0xffffffffu, w2, 1);
+                            double lp1 = __shfl_up_sync(0xffffffffu, p1, 1);
+                            double lp2 = __shfl_up_sync(0xffffffffu, p2, 1);
+                            lw1 = gl_on ? ga_cur : lw1;
+                            lw2 = gl_on ? ga_prev : lw2;
+                            lp1 = gl_on ? gb_cur : lp1;
+                            lp2 = gl_on ? gb_prev : lp2;
+                            double L[7];
+#pragma unroll
+                            for (int m = 0; m < 7; ++m) L[m] = rg[(j * 8 + m) * 32];
+                            const double r = rg[(j * 8 + 7) * 32];
+                            const double acc = fwd_chain<EXACT>(r, L, w1, p1, p0, lw2, lw1, lp2, lp1);
                             const bool vpt = tau >= lo && tau <= hi;
                             const double wnew = vpt ? acc : 0.0;
                             if (p_on && k > 0) sts(hin + ((tau + 1) & (HR - 1)) * 32, sentv());
@@ -732,6 +728,23 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                             const double *pv = pre + (tau & (PD - 1)) * 96;
                             if (q_on) q0 = gp_on ? pv[0] : lds_vol(hin + ((tau - 1) & (HR - 1)) * 32);
                             double ga_cur = pv[32], gb_cur = pv[64];
+                            // acquire: inputs produced by other warps must be final before the chain runs
+                            if (__any_sync(0xffffffffu,
+                                           (q_on && is_sent(q0)) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur))))) {
+                                long long spins = 0;
+                                for (;;) {
+                                    if (q_on && is_sent(q0)) q0 = gp_on ? ldg_cg(pw0 + tau * ZP)
+                                                                        : lds_vol(hin + ((tau - 1) & (HR - 1)) * 32);
+                                    if (gl_on) {
+                                        if (is_sent(ga_cur)) ga_cur = ldg_cg(pga + tau * ZP);
+                                        if (is_sent(gb_cur)) gb_cur = ldg_cg(pgb + tau * ZP);
+                                    }
+                                    const bool still =
+                                        (q_on && is_sent(q0)) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur)));
+                                    if (!__any_sync(0xffffffffu, still)) break;
+                                    if (++spins > (1ll << 26)) __trap();
+                                }
+                            }
                             double lw1 = __shfl_down_sync(0xffffffffu, wb1, 1);
                             double lw2 = __shfl_down_sync(0xffffffffu, wb2, 1);
                             double lq1 = __shfl_down_sync(0xffffffffu, q1, 1);
@@ -746,26 +759,7 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
 #pragma unroll
                             for (int m = 0; m < 7; ++m) Lq[m] = rg[(j * 8 + m) * 32];
                             const double inv_d = rg[(j * 8 + 7) * 32];
-                            double acc = bwd_chain<EXACT>(inv_d, wfv, Lq, wb1, q1, q0, lw2, lw1, lq2, lq1);
-                            const bool bad = (q_on && is_sent(q0)) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur)));
-                            if (__any_sync(0xffffffffu, bad)) {
-                                long long spins = 0;
-                                for (;;) {
-                                    if (q_on && is_sent(q0)) q0 = gp_on ? ldg_cg(pw0 + tau * ZP)
-                                                                        : lds_vol(hin + ((tau - 1) & (HR - 1)) * 32);
-                                    if (gl_on) {
-                                        if (is_sent(ga_cur)) ga_cur = ldg_cg(pga + tau * ZP);
-                                        if (is_sent(gb_cur)) gb_cur = ldg_cg(pgb + tau * ZP);
-                                    }
-                                    const bool still =
-                                        (q_on && is_sent(q0)) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur)));
-                                    if (!__any_sync(0xffffffffu, still)) break;
-                                    if (++spins > (1ll << 26)) __trap();
-                                }
-                                lw1 = gl_on ? ga_cur : lw1;
-                                lq1 = gl_on ? gb_cur : lq1;
-                                acc = bwd_chain<EXACT>(inv_d, wfv, Lq, wb1, q1, q0, lw2, lw1, lq2, lq1);
-                            }
+                            const double acc = bwd_chain<EXACT>(inv_d, wfv, Lq, wb1, q1, q0, lw2, lw1, lq2, lq1);
                             const bool vpt = tau >= lo && tau <= hi;
                             const double wnew = vpt ? acc : 0.0;
                             if (q_on && k > 0) sts(hin + ((tau - 1) & (HR - 1)) * 32, sentv());
