@@ -384,6 +384,9 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                 double *pwo = A.W + pidx(g, s, 0, z);
                 double *pbo = A.B + pidx(g, s, 0, z);
                 const bool gp_on = (k == 0), gl_on = (lane == 0);
+                // the global inputs can only be nonzero when the band below (b > 0) / the chunk below (c > 0)
+                // exists: otherwise they are boundary zeros and are neither fetched nor polled
+                const bool gp_ld = gp_on && b > 0, gl_ld = gl_on && z0 > 1;
                 // global handoff inputs of step tau, prefetched PD steps ahead into pre[k][tau & (PD-1)]
                 // (addresses of out-of-range steps stay inside the allocation and read boundary zeros)
                 double *pre = &S.pre[k][0][0][lane];
@@ -393,8 +396,8 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                 int tn = T0;
                 auto prefetch = [&]() {
                     const uint32_t d = pre_s + (uint32_t)((tn & (PD - 1)) * 96 * 8);
-                    if (gp_on) cpa8(d, nw0);
-                    if (gl_on) {
+                    if (gp_ld) cpa8(d, nw0);
+                    if (gl_ld) {
                         cpa8(d + 32 * 8, nga);
                         cpa8(d + 64 * 8, ngb);
                     }
@@ -427,21 +430,21 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                             double p0 = 0.0;
                             cpa_wait_pd();
                             const double *pv = pre + (tau & (PD - 1)) * 96;
-                            if (p_on) p0 = gp_on ? pv[0] : lds_vol(hin + ((tau + 1) & (HR - 1)) * 32);
-                            double ga_cur = pv[32], gb_cur = pv[64];
+                            if (p_on) p0 = gp_on ? (gp_ld ? pv[0] : 0.0) : lds_vol(hin + ((tau + 1) & (HR - 1)) * 32);
+                            double ga_cur = gl_ld ? pv[32] : 0.0, gb_cur = gl_ld ? pv[64] : 0.0;
                             // acquire: inputs produced by other warps must be final before the chain runs
                             if (__any_sync(0xffffffffu,
-                                           p_on && (is_sent(p0) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur)))))) {
+                                           p_on && (is_sent(p0) || (gl_ld && (is_sent(ga_cur) || is_sent(gb_cur)))))) {
                                 long long spins = 0;
                                 for (;;) {
                                     if (p_on && is_sent(p0)) p0 = gp_on ? ldg_cg(pw0 + tau * ZP)
                                                                         : lds_vol(hin + ((tau + 1) & (HR - 1)) * 32);
-                                    if (gl_on && p_on) {
+                                    if (gl_ld && p_on) {
                                         if (is_sent(ga_cur)) ga_cur = ldg_cg(pga + tau * ZP);
                                         if (is_sent(gb_cur)) gb_cur = ldg_cg(pgb + tau * ZP);
                                     }
                                     const bool still =
-                                        p_on && (is_sent(p0) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur))));
+                                        p_on && (is_sent(p0) || (gl_ld && (is_sent(ga_cur) || is_sent(gb_cur))));
                                     if (!__any_sync(0xffffffffu, still)) break;
                                     if (++spins > (1ll << 26)) __trap();
                                 }
@@ -691,14 +694,16 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                 double *pbo = A.B + pidx(g, s, 0, z);
                 double *pwo = A.W + pidx(g, s, 0, z);
                 const bool gp_on = (k == 0), gl_on = (lane == 31);
+                // nonzero only when the band above exists / row z0+32 exists on diagonal s or s+1
+                const bool gp_ld = gp_on && s0 + PW <= n - 2, gl_ld = gl_on && z0 + 32 <= s;
                 double *pre = &S.pre[k][0][0][lane];
                 const uint32_t pre_s = su32(pre);
                 const double *nw0 = pw0 + T1 * ZP, *nga = pga + T1 * ZP, *ngb = pgb + T1 * ZP;
                 int tn = T1;
                 auto prefetch = [&]() {
                     const uint32_t d = pre_s + (uint32_t)((tn & (PD - 1)) * 96 * 8);
-                    if (gp_on) cpa8(d, nw0);
-                    if (gl_on) {
+                    if (gp_ld) cpa8(d, nw0);
+                    if (gl_ld) {
                         cpa8(d + 32 * 8, nga);
                         cpa8(d + 64 * 8, ngb);
                     }
@@ -726,21 +731,21 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                             double q0 = 0.0;
                             cpa_wait_pd();
                             const double *pv = pre + (tau & (PD - 1)) * 96;
-                            if (q_on) q0 = gp_on ? pv[0] : lds_vol(hin + ((tau - 1) & (HR - 1)) * 32);
-                            double ga_cur = pv[32], gb_cur = pv[64];
+                            if (q_on) q0 = gp_on ? (gp_ld ? pv[0] : 0.0) : lds_vol(hin + ((tau - 1) & (HR - 1)) * 32);
+                            double ga_cur = gl_ld ? pv[32] : 0.0, gb_cur = gl_ld ? pv[64] : 0.0;
                             // acquire: inputs produced by other warps must be final before the chain runs
                             if (__any_sync(0xffffffffu,
-                                           (q_on && is_sent(q0)) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur))))) {
+                                           (q_on && is_sent(q0)) || (gl_ld && (is_sent(ga_cur) || is_sent(gb_cur))))) {
                                 long long spins = 0;
                                 for (;;) {
                                     if (q_on && is_sent(q0)) q0 = gp_on ? ldg_cg(pw0 + tau * ZP)
                                                                         : lds_vol(hin + ((tau - 1) & (HR - 1)) * 32);
-                                    if (gl_on) {
+                                    if (gl_ld) {
                                         if (is_sent(ga_cur)) ga_cur = ldg_cg(pga + tau * ZP);
                                         if (is_sent(gb_cur)) gb_cur = ldg_cg(pgb + tau * ZP);
                                     }
                                     const bool still =
-                                        (q_on && is_sent(q0)) || (gl_on && (is_sent(ga_cur) || is_sent(gb_cur)));
+                                        (q_on && is_sent(q0)) || (gl_ld && (is_sent(ga_cur) || is_sent(gb_cur)));
                                     if (!__any_sync(0xffffffffu, still)) break;
                                     if (++spins > (1ll << 26)) __trap();
                                 }
