@@ -17,21 +17,26 @@
 // stream per step, so every stream is one 256-byte coalesced segment, and the 15 stencil
 // neighbours of the residual come from three lines (s-1, s, s+1) at tau-2..tau+2.
 //
-// Bands.  A CTA (PW warps) processes one band task: PW consecutive diagonals s0..s0+PW-1 of one
-// 32-row chunk c.  Warp k owns diagonal s0+k and hands its values to warp k+1 through a
-// shared-memory ring (data is the flag: a signalling-NaN sentinel marks an empty slot; the
-// consumer re-arms the slot after reading it, the producer waits for an armed slot).  Across
+// Bands.  A CTA processes one band task: PW consecutive diagonals s0..s0+PW-1 of one 32-row chunk
+// c.  Per diagonal k the CTA runs a *solver* warp (the substitution chain and the handoffs only)
+// and helper warps that run ahead of it: forward, a march helper (the seven L values of every
+// point: NDDF march, V1 band rows or stored factors) and a residual helper (f - A u from 3D TMA
+// boxes of the u / f planes); backward, a march helper (the seven source-point L values and 1/D).
+// Helpers hand a group of GS steps at a time to their solver through a shared-memory ring with
+// mbarrier full / empty phases.  Solver k hands its values to solver k+1 through a shared-memory
+// ring in which the data is the flag (a signalling-NaN sentinel marks an empty slot; the consumer
+// re-arms the slot after reading it, the producer checks that its next slots are armed).  Across
 // bands (the band's first diagonal needs the previous band's last one) and across chunks (lane 0
 // needs row z0-1 of the chunk below) the values travel through global memory with the same
-// sentinel protocol on the handoff positions only:
+// sentinel protocol on the handoff positions only, prefetched PD steps ahead with cp.async:
 //   forward : W (w_f, full plane, written by the forward pass).  Handoff positions are the last
 //             diagonal of every band and the rows z = 0 mod 32.  The backward pass reads w_f and
 //             re-arms those positions.
 //   backward: B (w_b, handoff positions only: the first diagonal of every band and the rows
 //             z = 1 mod 32, z > 32).  The forward pass re-arms them.
-// Persistent CTAs take band tasks from one global ticket in a topological order (every task a
-// band depends on has a smaller ticket), so a CTA only waits for tasks held by running CTAs:
-// deadlock-free for any residency.
+// Persistent CTAs (one per SM) take band tasks from one global ticket in a topological order
+// (every task a band depends on has a smaller ticket), so a CTA only waits for tasks held by
+// running CTAs: deadlock-free for any residency.
 //
 // Per lane the arithmetic is exactly the reference's serial sequence for its row (NDDF seed table
 // in registers, marched after every point; residual in stencil_apply order; substitution in
