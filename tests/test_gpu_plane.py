@@ -144,3 +144,38 @@ def test_plane_config3_variable_coefficient():
     rn = plane_plan(level, src, fit, "v1").sweep(u, cuda(f), 3, norms=True)
     assert np.array_equal(u.cpu().numpy(), ref)
     np.testing.assert_allclose(rn.cpu().numpy().ravel(), nr, rtol=1e-12)
+
+
+def test_plane_level8_eight_chunks_bitwise():
+    """Level 8: diagonals of up to 253 rows (8 chunks of 32), 64 bands -- the cross-chunk and
+    cross-band handoffs at the scale of the level-9 runs."""
+    level = 8
+    src, fit, u0, f = case(level, 6, "v1", fseed=8)
+    ref, nr = oracle_sweeps(level, src, fit, "v1", u0, f, 2)
+    u = cuda(u0)
+    rn = plane_plan(level, src, fit, "v1").sweep(u, cuda(f), 2, norms=True)
+    assert np.array_equal(u.cpu().numpy(), ref)
+    np.testing.assert_allclose(rn.cpu().numpy().ravel(), nr, rtol=1e-12)
+
+
+def test_plane_two_streams_share_a_plan():
+    """Calls on two streams sharing one plan (and its plane workspace) serialise correctly."""
+    level = 6
+    src, fit, u0, f = case(level, 4, fseed=5)
+    p = plane_plan(level, src, fit, "v1")
+    ref = cuda(u0)
+    p.sweep(ref, cuda(f), 3)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    ua, ub = cuda(u0), cuda(u0 * 0.5)
+    fa, fb = cuda(f), cuda(f * 0.5)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        p.sweep(ua, fa, 3)
+    with torch.cuda.stream(s2):
+        p.sweep(ub, fb, 3)
+    torch.cuda.synchronize()
+    assert np.array_equal(ua.cpu().numpy(), ref.cpu().numpy())
+    ref_b = cuda(u0 * 0.5)
+    p.sweep(ref_b, cuda(f * 0.5), 3)
+    assert np.array_equal(ub.cpu().numpy(), ref_b.cpu().numpy())
