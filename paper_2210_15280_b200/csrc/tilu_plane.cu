@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
             const bool zr1 = z == 1, yr1 = y == 1, yr2 = y == 2, yge2 = y >= 2;
             // band / interior tests of the seven source points q_m = p - d_m (_lq, _kernels.py:434-441)
             // and of p (1/D).  Masks: bit m = q_m interior (m < 7); band bits in bmask (bit 7 = p).
-            auto tests = [&](int tau, unsigned &imask, unsigned &bmask, int (&o)[8]) {
+            auto tests = [&](int tau, unsigned &imask, unsigned &bmask) {
                 const int x = tau - z;
                 const bool vpt = tau >= lo && tau <= hi;
                 const bool x1 = x == 1, x2 = x == 2, xm1 = x == xe - 1, xm0 = x == xe;
@@ -845,6 +845,11 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                             (unsigned)(yge2 && (x1 || xm0 || yr2)) << 4 | (unsigned)(i1 && (x1 || xm1 || yr1)) << 5 |
                             (unsigned)(i2 && (x2 || xm0 || yr1)) << 6 | (unsigned)(x1 || xm0 || yr1 || zr1) << 7;
                 }
+            };
+            // store rows of the band source points (only evaluated when some lane has a band point)
+            auto offsets = [&](int tau, int (&o)[8]) {
+                const int x = tau - z;
+                const bool x1 = x == 1, x2 = x == 2;
                 o[0] = bo_own + ((zr1 || yr1) ? x : 1);
                 o[1] = bo_n + (zr1 ? x - 1 : (x1 ? 0 : 1));
                 o[2] = bo_n + (zr1 ? x - 2 : (x2 ? 0 : 1));
@@ -856,8 +861,7 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
             };
             // masks and band / factor values of step tau, computed GS steps ahead (one tests() per step)
             auto band_ld = [&](int tau, double(&v)[8], unsigned &im, unsigned &bm) {
-                int o[8];
-                tests(tau, im, bm, o);
+                tests(tau, im, bm);
                 if (stored) {  // factors of the source points q_m (transposed entries) and 1/D at p (_kernels.py:169-192)
                     const int x = tau - z;
                     const bool vp = tau >= lo && tau <= hi;
@@ -870,6 +874,8 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                     return;
                 }
                 if (__any_sync(0xffffffffu, bm != 0u)) {
+                    int o[8];
+                    offsets(tau, o);
 #pragma unroll
                     for (int m = 0; m < 8; ++m)
                         v[m] = ld_if((bm >> m) & 1u, P.store + 9 * (int64_t)o[m] + (m < 7 ? m : 8), 0.0);
