@@ -64,9 +64,15 @@ namespace pl {
 
 constexpr int PW = 4;    // diagonals per band (one solver warp + helper warps each)
 constexpr int GS = 4;    // steps per group: helper ring and TMA unit, unroll factor, global prefetch distance
-constexpr int NS = 2;    // helper -> solver ring depth (groups)
+#ifndef TILU_PLANE_NS
+#define TILU_PLANE_NS 2
+#endif
+constexpr int NS = TILU_PLANE_NS;  // helper -> solver ring depth (groups)
 constexpr int NT = 3;    // TMA ring depth (groups)
-constexpr int HR = 8;    // solver -> solver handoff ring depth (steps), power of two
+#ifndef TILU_PLANE_HR
+#define TILU_PLANE_HR 8
+#endif
+constexpr int HR = TILU_PLANE_HR;  // solver -> solver handoff ring depth (steps), power of two
 #ifndef TILU_PLANE_PD
 #define TILU_PLANE_PD 2
 #endif
