@@ -98,7 +98,11 @@ int tilu_stencil_apply(const tilu_plan_t *plan, const double *u, double *out, in
 /* `sweeps` smoothing steps u <- u + (L D L^T)^{-1}(f - A u) on every tet of the batch,
  * i.e. `sweeps` calls of the single-tet all-Dirichlet cell stage (multigrid.py:414-429 via
  * Hierarchy.smooth, :431-442).  u is updated in place; boundary entries are never written.
- * rnorm2 (DEVICE, [sweeps][ntets], may be NULL) receives ||f - A u||^2 before each sweep. */
+ * rnorm2 (DEVICE, [sweeps][ntets], may be NULL) receives ||f - A u||^2 before each sweep.
+ * Kernels: one tet from level 5 up -> plane-layout band kernels (the plan keeps a plane workspace of
+ * four vectors between calls; calls from several streams are serialised on it); several tets ->
+ * interleaved dataflow kernels; otherwise the reference-layout kernels.  All bitwise equal in exact
+ * mode. */
 int tilu_sweep(const tilu_plan_t *plan, double *u, const double *f, int ntets, int sweeps,
                double *rnorm2, void *stream);
 
@@ -109,8 +113,8 @@ int tilu_sweep(const tilu_plan_t *plan, double *u, const double *f, int ntets, i
  * zero).  tilu_sweep_packed() runs `sweeps` fused sweeps on packed u, f with caller-owned scratch
  * w_p of tilu_packed_scratch_size() doubles, zero-initialised before its first use (it keeps its
  * own state across calls: a header plus the two work vectors; reuse it only with the same plan and
- * ntets, or zero it again).  tilu_sweep() uses this path internally for ntets >= 2 and for single
- * tets from level 6 up. */
+ * ntets, or zero it again).  tilu_sweep() uses this path internally for ntets >= 2; single tets from
+ * level 5 up run on the plane-layout band kernels (see TILU_SCHED_PLANE / TILU_SCHED_BATCH). */
 int64_t tilu_packed_size(const tilu_plan_t *plan, int ntets);
 int64_t tilu_packed_scratch_size(const tilu_plan_t *plan, int ntets);
 int tilu_pack(const tilu_plan_t *plan, const double *src, double *dst, int ntets, void *stream);
