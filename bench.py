@@ -5,19 +5,27 @@ cubes x 6), each refined to level 7 (333,375 interior DoF per tet, 128,016,000 t
 Poisson, Dirichlet 0 on every macro-face, u ~ U[-1,1] (one global stream, seed 4, drawn in
 (tet, interior rank) order), f = 0, surrogate degree q = 6 (effective (4,4,5)), variant V1.
 It is the one configuration that spans 1-8 GPUs; the tets are partitioned contiguously
-across ranks (one process per GPU) with a per-sweep residual-norm allreduce (NCCL).
+across ranks (one process per GPU) with a per-sweep residual-norm allreduce (NCCL).  The L/U
+weights are evaluated on the fly by the NDDF march (the optional per-point coefficient tables,
+TILU_TAB=1, are never the headline).
 
 One step = one smoothing sweep (residual, forward L solve, D^-1 + backward L^T solve,
 update) over every tet of the rank, inputs resident in HBM (u, f are 1.1 GB each: larger
 than L2, so no flush is needed).  `e2e` = the same metric through the public API with
-pinned host buffers: H2D of u and f, `--e2e-sweeps` sweeps, D2H of u and the norms.
+pinned host buffers: every step H2D of u and f, one sweep, D2H of u and the norm
+(`e2e_multi`: 3 sweeps per host round trip).
 
-The line also carries `single_tet` (rank 0, N=1): one macro-tet at level 9 (configs[2] geometry
-and size, k = 1) through the plane-layout band kernels -- the north star's single-tet target --
-with its own roofline fraction, API-call time and e2e from pinned host buffers.
+The line also carries `config3` (rank 0, N=1): BASELINE.json configs[2] exactly -- the unit
+macro-tet at level 9 (22.1M DoF), k(x) = 1 + 0.5 sin(2 pi x) sin(2 pi y) sin(2 pi z) with the
+operator rows evaluated on the fly, f ~ N(0,1), u = 0, q = 6, 100 sweeps with the residual norm
+after each sweep -- through the plane-layout band kernels (the north star's single-GPU target),
+in exact (bitwise) and fast (FMA, <= 1e-12) mode, with its roofline and CPU baselines.
+
+CPU baselines: the reference's own Numba smoother (baseline/_ref/tetilu, installed from
+/root/reference; kind "reference") and the C restatement oracle/tilu_oracle.c (kind "port").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...
+    torchrun --nproc-per-node N bench.py --gpus N ...     (python bench.py --gpus N re-launches so)
 """
 
 from __future__ import annotations
@@ -35,11 +43,14 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 METRIC = "ILU(0) smoother DoF-updates/s (fwd+bwd sweep), 1–8 B200, % of roofline"
 UNIT = "DoF-updates/s"
 CFG4 = dict(tets=384, level=7, q=6, variant="v1", seed=4)
-HBM_FALLBACK = 6650.0
+CFG3 = dict(level=9, q=6, variant="v1", fseed=3, sweeps=100)
+HBM_FALLBACK = 6650.0     # B200_PROFILING.md fallback (GB/s) when MEASURED_PEAKS.json is absent
+FP64_FALLBACK = 37.0      # TF/s (FMA = 2), datasheet-class figure when profiles/fp64_peak.json is absent
 
 
 def log(*a):
@@ -49,6 +60,24 @@ def log(*a):
 # ----------------------------------------------------------------------------------------------
 # distributed plumbing
 # ----------------------------------------------------------------------------------------------
+def relaunch_under_torchrun(args) -> int | None:
+    """`python bench.py --gpus N` (N > 1, not already under torchrun): re-exec through
+    torch.distributed.run with N ranks on this node; NCCL_DEBUG=INFO makes the rank count visible."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    log("relaunching:", " ".join(cmd))
+    return subprocess.call(cmd, env=env)
+
+
 class Dist:
     def __init__(self, backend="nccl", init=True):
         import torch
@@ -75,13 +104,24 @@ class Dist:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t[0])
 
+    def info(self) -> dict:
+        if not self.dist:
+            return {"ranks": 1}
+        out = {"ranks": self.dist.get_world_size(), "backend": self.dist.get_backend()}
+        try:
+            v = self.torch.cuda.nccl.version()
+            out["nccl"] = ".".join(str(x) for x in v) if isinstance(v, tuple) else str(v)
+        except Exception:
+            pass
+        return out
+
     def close(self):
         if self.dist:
             self.dist.destroy_process_group()
 
 
 # ----------------------------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# clocks sampler (NVML during the timed region)
 # ----------------------------------------------------------------------------------------------
 class Clocks:
     """SM clock and throttle reasons sampled DURING the timed region: NVML (pynvml) every 2 ms on a
@@ -147,13 +187,24 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------------------------
-# workload
+# workload, roofline model
 # ----------------------------------------------------------------------------------------------
+def interior_mask(level: int) -> np.ndarray:
+    """Interior points of the full lattice in rank order (z, y, x), x, y, z >= 1, x+y+z <= n-1
+    (pure numpy: the reference arm must not import this package)."""
+    n = 2 ** level
+    out = []
+    for z in range(n + 1):
+        for y in range(n + 1 - z):
+            x = np.arange(n + 1 - z - y)
+            out.append((x >= 1) & (y >= 1) & (z >= 1) & (x + y + z <= n - 1))
+    return np.concatenate(out)
+
+
 def draw_u0(level: int, first_tet: int, ntets: int, seed: int) -> np.ndarray:
     """u0 for tets [first_tet, first_tet + ntets) of one global U[-1,1] stream drawn in
     (tet, interior rank) order -- independent of the GPU count."""
-    from paper_2210_15280_b200 import lattice
-    mask = lattice.interior_mask(level)
+    mask = interior_mask(level)
     nint = int(mask.sum())
     rng = np.random.default_rng(seed)
     rng.bit_generator.advance(first_tet * nint)
@@ -163,6 +214,13 @@ def draw_u0(level: int, first_tet: int, ntets: int, seed: int) -> np.ndarray:
     return u
 
 
+def config3_f(level: int) -> np.ndarray:
+    mask = interior_mask(level)
+    f = np.zeros(len(mask))
+    f[mask] = np.random.default_rng(CFG3["fseed"]).normal(size=int(mask.sum()))
+    return f
+
+
 def peaks() -> dict:
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -170,50 +228,76 @@ def peaks() -> dict:
         return {}
 
 
-def algo_bytes(level: int, nband: int, variant: str, shared_surrogate: bool = True) -> dict:
-    """Algorithmic bytes per interior DoF.  "sweep" is SURVEY 8(d)'s fixed model (vectors once per
-    pass, plus each tet's V1 band rows once per pass).  The per-kernel figures count what a kernel
-    must move: the batched kernels share ONE band store among all tets of a group (read once per
-    point, through the per-point coefficient table shared by every tet of the batch, L2-resident),
-    so their per-DoF band share is ~0; the sentinel re-arm writes (8 B/DoF per pass) are an
-    implementation overhead and are not counted."""
-    from paper_2210_15280_b200 import lattice
-    N = lattice.interior_size(level)
-    band = 72.0 * nband / N if variant == "v1" else 0.0
-    kb = 0.0 if shared_surrogate else band
-    return {
-        "sweep": 48.0 + 2 * band,
-        "batch_fwd": 24.0 + kb, "batch_bwd": 24.0 + kb,      # fused passes: u,f -> w ; w,u -> u
-        "residual": 24.0, "simple_fwd": 16.0 + band, "simple_bwd": 24.0 + band,
-    }
-
-
-def traffic_from_profiles(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu summary, or None."""
+def fp64_peak() -> tuple[float, float, str]:
+    """(FMA-counted TF/s, DADD Tops/s, source) from profiles/fp64_peak.json (tools/fp64_peak.cu,
+    measured on a B200 of this pool), else the fallback."""
     try:
-        tab = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        return tab.get(kernel)
+        d = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        return float(d["dfma_tflops"]), float(d["dadd_tops"]), "profiles/fp64_peak.json (measured)"
+    except (OSError, ValueError, KeyError):
+        return FP64_FALLBACK, FP64_FALLBACK / 2, "fallback (datasheet class)"
+
+
+def interior_count(level: int) -> int:
+    m = 2 ** level - 4
+    return (m + 1) * (m + 2) * (m + 3) // 6
+
+
+def band_count(level: int) -> int:
+    n = 2 ** level
+    k = 0
+    for z in range(1, n - 2):
+        for y in range(1, n - 1 - z):
+            xe = n - 1 - z - y
+            k += xe if (z == 1 or y == 1) else min(2, xe)
+    return k
+
+
+def algo_bytes(level: int, variant: str) -> dict:
+    """Algorithmic bytes per interior DoF (SURVEY 8(d) fixed model): the vectors once per pass
+    (fwd reads u, f, writes w; bwd reads w, u, writes u) + each tet's V1 band rows once per pass.
+    Per kernel: a fused pass moves 24 B/DoF of vectors + its band share."""
+    N = interior_count(level)
+    band = 72.0 * band_count(level) / N if variant == "v1" else 0.0
+    return {"sweep": 48.0 + 2 * band, "pass": 24.0 + band, "band_per_pass": band}
+
+
+def algo_ops(level: int, degrees) -> float:
+    """Algorithmic FP64 ops per interior DoF-update (every dmul / dadd / dsub = 1):
+    60 + 15 kx per point, + per-row seeding 15 [(kx+1) 2 ky + cnt (2 kx + 1) + cnt (cnt - 1) / 2]
+    + per-layer collapse 15 (kx+1)(ky+1) 2 kz."""
+    kx, ky, kz = (int(d) for d in degrees)
+    n = 2 ** level
+    N = interior_count(level)
+    tot = float(N) * (60 + 15 * kx)
+    for z in range(1, n - 2):
+        for y in range(1, n - 1 - z):
+            cnt = min(kx + 1, n - 1 - z - y)
+            tot += 15 * ((kx + 1) * 2 * ky + cnt * (2 * kx + 1) + cnt * (cnt - 1) / 2)
+    tot += (n - 3) * 15 * (kx + 1) * (ky + 1) * 2 * kz
+    return tot / N
+
+
+def roofline_time(dofs: float, bytes_per_dof: float, ops_per_dof: float) -> dict:
+    """max(bytes at HBM bandwidth, FP64 ops at peak) for one sweep of `dofs` DoF."""
+    pk = peaks()
+    hbm = pk.get("hbm_gbs") or HBM_FALLBACK
+    tf, dadd, src64 = fp64_peak()
+    t_hbm = dofs * bytes_per_dof / (hbm * 1e9)
+    t_fp = dofs * ops_per_dof / (tf * 1e12)
+    return {"t_hbm_s": t_hbm, "t_fp64_s": t_fp, "t_fp64_issue_s": dofs * ops_per_dof / (dadd * 1e12),
+            "bound": "hbm" if t_hbm >= t_fp else "fp64", "hbm_gbs": hbm, "fp64_tflops": tf,
+            "hbm_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if pk.get("hbm_gbs") else
+                          "B200_PROFILING.md fallback", "fp64_source": src64}
+
+
+def ncu_table(name: str) -> dict:
+    """Per-kernel ncu figures from the committed summary (profiles/ncu_kernels.json): dram bytes per
+    launch and FP64 pipe utilisation of the latest capture, or {}."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_kernels.json"))).get(name, {})
     except (OSError, ValueError):
-        return None
-
-
-# ----------------------------------------------------------------------------------------------
-# CPU baseline (oracle port) -- test infrastructure, never the product path
-# ----------------------------------------------------------------------------------------------
-def cpu_reference(fit, src, level: int, ntets_sample: int, threads: int, sweeps: int = 1) -> dict:
-    from oracle import oracle as O
-    from paper_2210_15280_b200 import lattice
-    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, fit.variant, fit.band_ranks, fit.store_rows)
-    u = draw_u0(level, 0, ntets_sample, CFG4["seed"])
-    f = np.zeros_like(u)
-    t0 = time.perf_counter()
-    used = O.sweeps_many(sur, level, np.atleast_1d(src.data), u, f, sweeps, nthreads=threads)
-    dt = time.perf_counter() - t0
-    dofs = lattice.interior_size(level) * ntets_sample * sweeps
-    return {"value": dofs / dt, "unit": UNIT, "cores": used, "kind": "port", "seconds": dt,
-            "sample": f"{ntets_sample} Kuhn tets x {sweeps} sweep (L{level}, q=6 eff {tuple(fit.degrees)}, V1): "
-                      f"oracle/tilu_oracle.c (serial C restatement of the reference Numba sweep), one OpenMP "
-                      f"thread per tet"}
+        return {}
 
 
 def host_threads() -> int:
@@ -223,46 +307,13 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def build_config4_fit():
-    from paper_2210_15280_b200 import fitting, lattice, stencil
-    src = stencil.stencil_source(lattice.kuhn_tet((0, 1, 2)), CFG4["level"], stencil.CoefficientField.constant(1.0))
-    q = CFG4["q"]
-    return src, fitting.fit_surrogate_ilu(src, CFG4["level"], (q, q, q), CFG4["variant"])
-
-
-def run_reference(args, D: Dist):
-    """--impl reference: the reference's CPU sweep (oracle port, all host threads), rank 0 only."""
-    if D.rank != 0:
-        return
-    src, fit = build_config4_fit()
-    threads = host_threads()
-    nt = min(CFG4["tets"], max(threads, 8))
-    for _ in range(args.warmup):
-        cpu_reference(fit, src, CFG4["level"], nt, threads)
-    vals = [cpu_reference(fit, src, CFG4["level"], nt, threads) for _ in range(args.steps)]
-    secs = sum(v["seconds"] for v in vals)
-    dofs_step = vals[0]["value"] * vals[0]["seconds"]
-    value = dofs_step * len(vals) / secs
-    cb = dict(vals[0])
-    cb.pop("seconds")
-    cb["value"] = value
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / len(vals),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(fit, 1, extra={"sample_tets_per_step": nt}),
-        "cpu_baseline": cb, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def config_block(fit, world, extra=None) -> dict:
-    from paper_2210_15280_b200 import lattice
+def config_block(degrees, world, extra=None) -> dict:
     c = {
         "workload": "configs[3]: 384 Kuhn macro-tets (4x4x4 unit cubes x 6), level 7 each, Poisson, "
                     "Dirichlet 0, u~U[-1,1] seed 4, f=0, q=6, V1; one step = one sweep over all tets",
-        "tets": CFG4["tets"], "level": CFG4["level"], "dofs": CFG4["tets"] * lattice.interior_size(CFG4["level"]),
-        "q": CFG4["q"], "effective_degrees": list(fit.degrees), "variant": CFG4["variant"],
+        "tets": CFG4["tets"], "level": CFG4["level"], "dofs": CFG4["tets"] * interior_count(CFG4["level"]),
+        "q": CFG4["q"], "effective_degrees": list(degrees), "variant": CFG4["variant"],
+        "coefficients": "L/U weights evaluated on the fly (NDDF march), no stored factor / table",
         "parallelism": f"macro-tet partition x{world}, NCCL residual-norm allreduce per sweep",
         "l2": "inputs larger than L2 (u, f 1.1 GB each); no flush needed",
     }
@@ -272,77 +323,289 @@ def config_block(fit, world, extra=None) -> dict:
 
 
 # ----------------------------------------------------------------------------------------------
+# CPU baselines -- test infrastructure, never the product path
+# ----------------------------------------------------------------------------------------------
+_NB = {}   # state of the Numba reference workers (set before the pool forks)
+
+
+def _ref_import():
+    """The UNMODIFIED reference (pip-installed from /root/reference into baseline/_ref)."""
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import tetilu  # noqa: F401
+    from tetilu import _kernels, geometry
+    from tetilu.assembly import CoefficientField, stencil_source
+    from tetilu.surrogate import build_surrogate_ilu
+    return _kernels, geometry, CoefficientField, stencil_source, build_surrogate_ilu
+
+
+def _nb_sweeps(task):
+    """One tet, `sweeps` cell stages of the reference (multigrid.py:414-429 in stencil form):
+    r = f - A u (_kernels.stencil_apply), w[interior] = r, SurrogateILU.solve_into(w), u += w."""
+    t, sweeps = task
+    _kernels = _NB["kernels"]
+    pre, arows, aconst, n, rowoff, mask = _NB["pre"], _NB["arows"], _NB["aconst"], _NB["n"], _NB["rowoff"], _NB["mask"]
+    u = draw_u0(_NB["level"], t, 1, CFG4["seed"])[0] if _NB.get("u") is None else _NB["u"].copy()
+    f = np.zeros_like(u) if _NB.get("f") is None else _NB["f"]
+    out = np.zeros_like(u)
+    w = np.zeros_like(u)
+    t0 = time.perf_counter()
+    for _ in range(sweeps):
+        _kernels.stencil_apply(n, rowoff, arows, aconst, u, out)
+        w[:] = 0.0
+        w[mask] = f[mask] - out[mask]
+        pre.solve_into(w)
+        u[mask] += w[mask]
+    return time.perf_counter() - t0
+
+
+def numba_config4(ntets: int, sweeps: int, procs: int) -> dict:
+    """The reference's own CPU smoother on config-4 tets: reference setup (stencil_source +
+    build_surrogate_ilu of one Kuhn tet; all 384 share the operator), one Numba JIT warm-up, then a
+    fork pool over `procs` host cores, one tet per task (the reference kernels are serial)."""
+    import multiprocessing as mp
+    _kernels, geometry, CF, ssrc, build = _ref_import()
+    level, q = CFG4["level"], CFG4["q"]
+    t0 = time.time()
+    kuhn = np.array([(0, 0, 0), (1, 0, 0), (1, 1, 0), (1, 1, 1)], dtype=float)
+    tet = geometry.MacroTet(kuhn) if hasattr(geometry, "MacroTet") else kuhn
+    src = ssrc(tet, level, CF.constant(1.0))
+    pre = build(src, level, (q, q, q), variant=CFG4["variant"])
+    arows, aconst = src.kernel_args
+    n = 2 ** level
+    _NB.update(kernels=_kernels, pre=pre, arows=arows, aconst=aconst, n=n, rowoff=pre._rowoff, level=level,
+               mask=interior_mask(level), u=None, f=None)
+    setup = time.time() - t0
+    _nb_sweeps((0, 1))  # JIT (cache=True) before the fork
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        pool.map(_nb_sweeps, [(i, 1) for i in range(procs)])  # warm the workers
+        t1 = time.perf_counter()
+        pool.map(_nb_sweeps, [(i, sweeps) for i in range(ntets)], chunksize=1)
+        dt = time.perf_counter() - t1
+    dofs = interior_count(level) * ntets * sweeps
+    return {"value": dofs / dt, "unit": UNIT, "cores": procs, "kind": "reference", "seconds": dt,
+            "setup_s": setup,
+            "sample": f"{ntets} Kuhn tets x {sweeps} sweep (L{level}, q={q}, V1): the reference's Numba "
+                      f"cell stage (baseline/_ref/tetilu: stencil_apply + SurrogateILU.solve_into + update), "
+                      f"fork pool of {procs} processes, one tet per task"}
+
+
+def port_config4(ntets: int, sweeps: int, threads: int, fitz=None) -> dict:
+    """The C restatement (oracle/tilu_oracle.c) on config-4 tets, one OpenMP thread per tet.  The
+    fitted arrays come from `fitz` (this repo's setup) or the committed bench_data/cfg4_L7_fit.npz."""
+    from oracle import oracle as O
+    level = CFG4["level"]
+    if fitz is None:
+        fitz = dict(np.load(os.path.join(ROOT, "bench_data", "cfg4_L7_fit.npz")))
+    sur = O.OracleSurrogate(level, fitz["lcoefs"], fitz["dcoefs"], CFG4["variant"], fitz["band_ranks"],
+                            fitz["store_rows"])
+    u = draw_u0(level, 0, ntets, CFG4["seed"])
+    f = np.zeros_like(u)
+    t0 = time.perf_counter()
+    used = O.sweeps_many(sur, level, np.atleast_1d(fitz["arow"]), u, f, sweeps, nthreads=threads)
+    dt = time.perf_counter() - t0
+    dofs = interior_count(level) * ntets * sweeps
+    return {"value": dofs / dt, "unit": UNIT, "cores": used, "kind": "port", "seconds": dt,
+            "sample": f"{ntets} Kuhn tets x {sweeps} sweep (L{level}, q=6, V1): oracle/tilu_oracle.c (serial C "
+                      f"restatement of the reference Numba sweep), one OpenMP thread per tet"}
+
+
+def run_reference(args, D: Dist):
+    """--impl reference: the reference's own CPU smoother (Numba, baseline/_ref) on config 4's workload
+    sample with all host cores; rank 0 only.  Never imports this repo's package.  Falls back to the
+    C port (with the committed fitted arrays) if the reference cannot be imported on this host."""
+    if D.rank != 0:
+        return
+    cores = host_threads()
+    nt = min(CFG4["tets"], 2 * cores)
+    try:
+        runs = []
+        for i in range(args.warmup + args.steps):
+            r = numba_config4(nt, 1, cores) if i == 0 else _numba_again(nt, cores)
+            if i >= args.warmup:
+                runs.append(r)
+    except Exception as e:  # reference not importable here: the port stands in, and says so
+        log(f"reference import failed ({type(e).__name__}: {e}); timing the C port instead")
+        runs = [port_config4(nt, 1, cores) for _ in range(args.warmup + args.steps)][args.warmup:]
+    secs = sum(r["seconds"] for r in runs)
+    value = interior_count(CFG4["level"]) * nt * len(runs) / secs
+    cb = {k: v for k, v in runs[0].items() if k not in ("seconds", "setup_s")}
+    cb["value"] = value
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / len(runs),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block((4, 4, 5), 1, extra={"sample_tets_per_step": nt,
+                                                    "note": "each step = one sweep over a sample of "
+                                                            f"{nt} of the 384 tets (same per-tet work)"}),
+        "cpu_baseline": cb, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _numba_again(nt: int, cores: int) -> dict:
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_nb_sweeps, [(i, 1) for i in range(cores)])
+        t1 = time.perf_counter()
+        pool.map(_nb_sweeps, [(i, 1) for i in range(nt)], chunksize=1)
+        dt = time.perf_counter() - t1
+    return {"value": interior_count(CFG4["level"]) * nt / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+            "seconds": dt, "sample": f"{nt} Kuhn tets x 1 sweep, Numba reference, fork pool of {cores}"}
+
+
+def numba_config3_sweep(fit, src, f: np.ndarray) -> dict:
+    """One config-3 cell stage (level 9) of the reference's Numba kernels on this repo's fitted
+    arrays and per-point rows (bitwise the reference's own setup's rows; its ~30 min level-9 setup
+    is not repeated here): stencil_apply + surrogate_forward/backward + update, 1 core."""
+    _kernels, *_ = _ref_import()
+    from paper_2210_15280_b200 import lattice
+    level = CFG3["level"]
+    n = 2 ** level
+    rowoff = np.ascontiguousarray(lattice.rank_tables(level))
+    lc, dc = np.ascontiguousarray(fit.lcoefs), np.ascontiguousarray(fit.dcoefs)
+    br, sr = np.ascontiguousarray(fit.band_ranks), np.ascontiguousarray(fit.store_rows)
+    mask = lattice.interior_mask(level)
+    u, out, w = np.zeros_like(f), np.zeros_like(f), np.zeros_like(f)
+    arows = np.atleast_2d(src.data)
+
+    def stage():
+        _kernels.stencil_apply(n, rowoff, arows, False, u, out)
+        w[:] = 0.0
+        w[mask] = f[mask] - out[mask]
+        _kernels.surrogate_forward(n, rowoff, 1.0 / n, lc, w, True, br, sr)
+        _kernels.surrogate_backward(n, rowoff, 1.0 / n, lc, dc, w, True, br, sr)
+        u[mask] += w[mask]
+
+    # JIT warm-up on a small level would change the signature's cache entry only by shape: warm on L9
+    t0 = time.perf_counter()
+    stage()
+    jit_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    stage()
+    dt = time.perf_counter() - t0
+    N = interior_count(level)
+    return {"value": N / dt, "unit": UNIT, "cores": 1, "kind": "reference", "seconds": dt, "first_call_s": jit_s,
+            "sample": "1 config-3 sweep at level 9 (22.1M DoF) after one warm-up sweep: the reference's Numba "
+                      "stencil_apply + surrogate_forward/backward + update (baseline/_ref/tetilu; serial), on this "
+                      "repo's fitted arrays and per-point rows"}
+
+
+def port_config3_sweep(fit, src, f: np.ndarray) -> dict:
+    from oracle import oracle as O
+    level = CFG3["level"]
+    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows)
+    u = np.zeros_like(f)
+    t0 = time.perf_counter()
+    O.sweeps(sur, level, src.data, u, f, 1)
+    dt = time.perf_counter() - t0
+    return {"value": interior_count(level) / dt, "unit": UNIT, "cores": 1, "kind": "port", "seconds": dt,
+            "sample": "1 config-3 sweep at level 9 (22.1M DoF): oracle/tilu_oracle.c, serial"}
+
+
+# ----------------------------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------------------------
-def run_single(args) -> dict:
-    """One macro-tet at the north star's level (configs[2] geometry and size: unit tet, level 9,
-    q = 6 -> effective (4, 4, 4), V1, f ~ N(0, 1), u = 0) through the plane-layout band kernels.
-    The coefficient is k = 1 (constant stencil): config 3's variable k(x) needs the per-point
-    stencil assembled on the host (28 min in the reference) and a per-point residual; the sweep
-    kernels are the same.  Reported: device time per sweep of the two plane kernels (resident,
-    `value`), the API call time (pack + sweeps + unpack + norms per call), and e2e from pinned host
-    buffers (H2D u, f -> sweeps -> D2H u)."""
+def run_config3(args) -> dict:
+    """BASELINE.json configs[2] on one GPU through the plane-layout band kernels, operator rows on
+    the fly (no per-point rows on the device).  One call = 100 sweeps with the residual norm
+    ||f - A u||^2 before every sweep (fused into the forward pass: the norm after sweep k is the one
+    before sweep k+1) + one residual after the last sweep."""
     import torch
 
     from paper_2210_15280_b200 import DevicePlan, _lib, fitting, lattice, stencil
-    level, q, sweeps = args.single_level, 6, args.single_sweeps
+    level, q, sweeps = CFG3["level"], CFG3["q"], args.config3_sweeps
     t0 = time.time()
-    src = stencil.stencil_source(lattice.unit_tet(), level, stencil.CoefficientField.constant(1.0))
-    fit = fitting.fit_surrogate_ilu(src, level, (q, q, q), "v1")
+    src = stencil.stencil_source(lattice.unit_tet(), level, stencil.sin_kappa())
+    fit = fitting.fit_surrogate_ilu(src, level, (q, q, q), CFG3["variant"])
     setup_s = time.time() - t0
     N = lattice.interior_size(level)
-    mask = lattice.interior_mask(level)
-    f_host = np.zeros(lattice.grid_size(level))
-    f_host[mask] = np.random.default_rng(3).normal(size=int(mask.sum()))
+    f_host = config3_f(level)
     dev = torch.device("cuda", torch.cuda.current_device())
-    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data,
-                   fast=args.fast)
     f = torch.as_tensor(f_host, device=dev)
-    u = torch.zeros_like(f)
-    p.sweep(u, f, 3)  # warm-up (workspace, arming, clocks)
-    torch.cuda.synchronize()
-    u.zero_()
-    _lib.profile_enable(True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    rn = p.sweep(u, f, sweeps, norms=True)
-    e1.record()
-    torch.cuda.synchronize()
-    kprof = _lib.profile_read()
-    _lib.profile_enable(False)
-    call_ms = e0.elapsed_time(e1) / sweeps
-    kern_ms = sum(tot for name, (cnt, tot) in kprof.items() if name in ("plane_fwd", "plane_bwd")) / sweeps
-    ab = algo_bytes(level, len(fit.band_ranks), "v1")["sweep"]
-    pk = peaks()
-    peak = pk.get("hbm_gbs") or HBM_FALLBACK
-    achieved = ab * N / (kern_ms / 1e3) / 1e9
-    # e2e: pinned host u, f -> device -> sweeps -> host u
-    uh = torch.zeros(f.numel(), dtype=torch.float64).pin_memory()
-    fh = torch.from_numpy(f_host).pin_memory()
-    torch.cuda.synchronize()
-    e0.record()
-    ud = uh.to(dev, non_blocking=True)
-    fd = fh.to(dev, non_blocking=True)
-    p.sweep(ud, fd, sweeps)
-    uh.copy_(ud, non_blocking=True)
-    e1.record()
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    rho = float((rn[-1] / rn[-2]).sqrt()) if sweeps >= 2 else None
-    return {
-        "workload": f"configs[2] geometry/size with k=1: unit macro-tet, level {level} ({N} interior DoF), "
-                    f"q=6 eff {tuple(fit.degrees)}, V1, f~N(0,1) seed 3, u=0, {sweeps} sweeps per call",
-        "value": N / (kern_ms / 1e3), "unit": UNIT, "ms_per_sweep_kernels": kern_ms,
-        "ms_per_sweep_call": call_ms, "api_value": N / (call_ms / 1e3),
-        "roofline": {"bound": "hbm", "algorithmic_bytes_per_dof": ab, "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak},
-        "e2e": {"value": N * sweeps / (e2e_ms / 1e3), "unit": UNIT, "ms": e2e_ms,
-                "h2d_bytes_per_step": 2 * f.numel() * 8, "d2h_bytes_per_step": f.numel() * 8,
-                "sweeps_per_step": sweeps, "api": "DevicePlan.sweep on device copies of pinned host u, f"},
-        "kernels": {k: {"launches": c, "avg_ms": t / c} for k, (c, t) in kprof.items()},
-        "residual_ratio_last": rho, "setup_s": setup_s,
-        "mode": "fast (FMA)" if args.fast else "exact (bitwise)",
-    }
+    ab = algo_bytes(level, "v1")
+    ops = algo_ops(level, fit.degrees)
+    # fixed model: the trailing residual (reads u, f: 16 B/DoF, 30 ops) amortised over the call's sweeps
+    call_bytes = ab["sweep"] + 16.0 / sweeps
+    call_ops = ops + 30.0 / sweeps
+    roof = roofline_time(N, call_bytes, call_ops)
+    t100 = max(roof["t_hbm_s"], roof["t_fp64_s"])
+    out = {"workload": f"configs[2]: unit macro-tet, level {level} ({N} interior DoF), k(x)=1+0.5 sin(2 pi x) "
+                       f"sin(2 pi y) sin(2 pi z) (rows on the fly), f~N(0,1) seed {CFG3['fseed']}, u=0, q={q} eff "
+                       f"{tuple(fit.degrees)}, V1, {sweeps} sweeps + residual norm after each",
+           "unit": UNIT, "setup_s": setup_s, "algorithmic_bytes_per_dof": call_bytes,
+           "algorithmic_fp64_ops_per_dof": call_ops}
+    for mode, fast in (("exact", False), ("fast", True)):
+        p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, sepk=src.sepk, fast=fast)
+        u = torch.zeros_like(f)
+        p.sweep(u, f, 3)  # warm-up (workspace, arming, clocks)
+        torch.cuda.synchronize()
+        u.zero_()
+        _lib.profile_enable(True)
+        clocks = Clocks(torch.cuda.current_device())
+        clocks.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rn = p.sweep(u, f, sweeps, norms=True)
+        _, rfin = p.residual(u, f, norms=True)
+        e1.record()
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+        kprof = _lib.profile_read()
+        _lib.profile_enable(False)
+        ms = e0.elapsed_time(e1)
+        kern_ms = sum(tot for name, (cnt, tot) in kprof.items() if name in ("plane_fwd", "plane_bwd")) / sweeps
+        fwd = kprof.get("plane_fwd", (1, 0.0))
+        pass_bytes = ab["pass"] * N
+        r = {
+            "value": N * sweeps / (ms / 1e3), "ms_per_sweep": ms / sweeps, "ms_per_sweep_kernels": kern_ms,
+            "roofline": {"bound": roof["bound"], "frac": t100 / (ms / 1e3 / sweeps),
+                         "achieved": call_bytes * N * sweeps / (ms / 1e3) / 1e9, "peak": roof["hbm_gbs"],
+                         "unit": "GB/s", "t_roofline_ms": t100 * 1e3, "t_hbm_ms": roof["t_hbm_s"] * 1e3,
+                         "t_fp64_ms": roof["t_fp64_s"] * 1e3, "fp64_tflops_peak": roof["fp64_tflops"],
+                         "fp64_achieved_tflops": call_ops * N * sweeps / (ms / 1e3) / 1e12},
+            "dominant_kernel": {"name": "plane_fwd", "avg_ms": fwd[1] / max(fwd[0], 1),
+                                "achieved_gbs": pass_bytes / (fwd[1] / max(fwd[0], 1) / 1e3) / 1e9,
+                                "frac": pass_bytes / (fwd[1] / max(fwd[0], 1) / 1e3) / 1e9 / roof["hbm_gbs"],
+                                **ncu_table("plane_fwd")},
+            "kernels": {k: {"launches": c, "avg_ms": t / c} for k, (c, t) in kprof.items()},
+            "residual_norm2_after": [float(x) for x in rn.cpu().numpy().ravel()[1:4]] + [float(rfin[0])],
+            "rate_last": float(np.sqrt(float(rfin[0]) / float(rn[-1, 0]))),
+            "clocks": clk, "mode": "exact (bitwise vs the oracle)" if not fast else "fast (FMA; <= 1e-12 vs the oracle)",
+        }
+        if not fast:
+            # e2e: pinned host u, f -> device -> sweeps + residual -> host u and norms
+            uh = torch.zeros(f.numel(), dtype=torch.float64).pin_memory()
+            fh = torch.from_numpy(f_host).pin_memory()
+            torch.cuda.synchronize()
+            e0.record()
+            ud = uh.to(dev, non_blocking=True)
+            fd = fh.to(dev, non_blocking=True)
+            rn2 = p.sweep(ud, fd, sweeps, norms=True)
+            _, rf2 = p.residual(ud, fd, norms=True)
+            uh.copy_(ud, non_blocking=True)
+            nh = torch.cat([rn2.ravel(), rf2]).to("cpu", non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            e2e_ms = e0.elapsed_time(e1)
+            r["e2e"] = {"value": N * sweeps / (e2e_ms / 1e3), "unit": UNIT, "ms": e2e_ms,
+                        "h2d_bytes_per_step": 2 * f.numel() * 8, "d2h_bytes_per_step": f.numel() * 8 + nh.numel() * 8,
+                        "sweeps_per_step": sweeps,
+                        "api": "DevicePlan.sweep(norms) + residual on device copies of pinned host u, f"}
+        out[mode] = r
+        del p
+    out["value"] = out["exact"]["value"]
+    # CPU baselines on the same workload (bounded samples: one level-9 sweep each)
+    if not args.no_cpu:
+        out["cpu_baseline"] = []
+        try:
+            out["cpu_baseline"].append({k: v for k, v in numba_config3_sweep(fit, src, f_host).items()})
+        except Exception as e:
+            out["cpu_baseline"].append({"kind": "reference", "unavailable": f"{type(e).__name__}: {e}"})
+        out["cpu_baseline"].append(port_config3_sweep(fit, src, f_host))
+    return out
 
 
 def run_ours(args, D: Dist):
@@ -395,84 +658,107 @@ def run_ours(args, D: Dist):
     _lib.profile_enable(False)
     launches = mm.launches
     ms = D.max(ms_local)
-    dofs_total = CFG4["tets"] * lattice.interior_size(level)
+    N = interior_count(level)
+    dofs_total = CFG4["tets"] * N
     value = dofs_total * args.steps / (ms / 1e3)
 
-    # dominant kernel roofline
-    ab = algo_bytes(level, len(fit.band_ranks), CFG4["variant"])
-    pk = peaks()
-    peak = pk.get("hbm_gbs") or HBM_FALLBACK
+    # roofline: the sweep (fixed model) and the dominant kernel
+    ab = algo_bytes(level, CFG4["variant"])
+    ops = algo_ops(level, fit.degrees)
+    roof_t = roofline_time(dofs_total / D.world, ab["sweep"], ops)
+    t_roof = max(roof_t["t_hbm_s"], roof_t["t_fp64_s"])
+    sweep_ms = ms / args.steps
     dom = max(kprof.items(), key=lambda kv: kv[1][1]) if kprof else None
     roof = None
     if dom is not None:
         name, (cnt, tot) = dom
         per_launch_ms = tot / cnt
-        bytes_per_launch = ab.get(name, ab["sweep"]) * lattice.interior_size(level) * len(local)
+        bytes_per_launch = ab["pass"] * N * len(local)
         achieved = bytes_per_launch / (per_launch_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic_from_profiles(name),
+        nc = ncu_table(name)
+        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": roof_t["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / roof_t["hbm_gbs"], "traffic": nc.get("dram_bytes_per_launch"),
+                "fp64_pipe_pct": nc.get("fp64_pipe_pct"), "ncu_source": nc.get("source"),
                 "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": per_launch_ms,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if pk.get("hbm_gbs") else
-                               "B200_PROFILING.md fallback (of fallback)",
-                "step_share": tot / ms_local if ms_local else None}
-    sweep_ms = ms / args.steps
-    sweep_achieved = ab["sweep"] * dofs_total / D.world / (sweep_ms / 1e3) / 1e9
+                "peak_source": roof_t["hbm_source"], "step_share": tot / ms_local if ms_local else None}
     kernels = {k: {"launches": c, "avg_ms": t / c} for k, (c, t) in kprof.items()}
 
-    # e2e through the public API with pinned host buffers
-    e2e = None
+    # e2e through the public API with pinned host buffers: one sweep per host round trip (strict),
+    # and three (amortised)
+    e2e, e2e_multi = None, None
     if args.e2e_sweeps > 0:
         uh = torch.from_numpy(u_host).pin_memory()
         fh = torch.zeros_like(uh).pin_memory()
-        mm.apply_host(uh.clone().pin_memory(), fh, args.e2e_sweeps, chunk=args.e2e_chunk)  # warm
-        torch.cuda.synchronize()
-        D.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = max(1, min(args.steps, 3))
-        e0.record()
-        for _ in range(reps):
-            mm.apply_host(uh, fh, args.e2e_sweeps, chunk=args.e2e_chunk)
-        e1.record()
-        torch.cuda.synchronize()
-        D.barrier()
-        ems = D.max(e0.elapsed_time(e1)) / reps
-        h2d = 2 * uh.numel() * 8
-        d2h = uh.numel() * 8 + 8 * args.e2e_sweeps
-        e2e = {"value": dofs_total * args.e2e_sweeps / (ems / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": h2d * D.world, "d2h_bytes_per_step": d2h * D.world,
-               "sweeps_per_step": args.e2e_sweeps, "ms_per_step": ems,
-               "api": f"MacroMeshSmoother.apply_host(pinned u, f, sweeps): {args.e2e_chunk}-tet chunks "
-                      f"pipelined on 2 streams (H2D / sweeps / D2H overlap)"}
+        for sw in (1, args.e2e_sweeps):
+            mm.apply_host(uh.clone().pin_memory(), fh, sw, chunk=args.e2e_chunk)  # warm
+            torch.cuda.synchronize()
+            D.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(1, min(args.steps, 3))
+            e0.record()
+            for _ in range(reps):
+                mm.apply_host(uh, fh, sw, chunk=args.e2e_chunk)
+            e1.record()
+            torch.cuda.synchronize()
+            D.barrier()
+            ems = D.max(e0.elapsed_time(e1)) / reps
+            h2d = 2 * uh.numel() * 8
+            d2h = uh.numel() * 8 + 8 * sw
+            rec = {"value": dofs_total * sw / (ems / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": h2d * D.world, "d2h_bytes_per_step": d2h * D.world,
+                   "sweeps_per_step": sw, "ms_per_step": ems,
+                   "api": f"MacroMeshSmoother.apply_host(pinned u, f, sweeps={sw}): {args.e2e_chunk}-tet chunks "
+                          f"pipelined on 2 streams (H2D / sweeps / D2H overlap)"}
+            if sw == 1:
+                e2e = rec
+            else:
+                e2e_multi = rec
 
-    # CPU baseline (rank 0, N=1 only)
-    cpu = None
+    # CPU baselines (rank 0, N=1 only): the reference's Numba smoother and the C port
+    cpu, cpu_port = None, None
     if D.world == 1 and D.rank == 0 and not args.no_cpu:
-        threads = host_threads()
-        src = mm.smoothers[0].source
-        nt = min(CFG4["tets"], max(threads, 8))
-        cpu = cpu_reference(fit, src, level, nt, threads)
-        cpu.pop("seconds")
+        cores = host_threads()
+        nt = min(CFG4["tets"], 2 * cores)
+        try:
+            cpu = numba_config4(nt, 1, cores)
+            cpu.pop("seconds")
+        except Exception as e:
+            cpu = {"kind": "reference", "unavailable": f"{type(e).__name__}: {e}"}
+        sm = mm.smoothers[0]
+        fitz = dict(lcoefs=fit.lcoefs, dcoefs=fit.dcoefs, band_ranks=fit.band_ranks, store_rows=fit.store_rows,
+                    arow=np.atleast_1d(sm.source.data))
+        cpu_port = port_config4(nt, 1, cores, fitz)
+        cpu_port.pop("seconds")
+        if "unavailable" in cpu:
+            cpu, cpu_port = cpu_port, cpu
 
-    single = None
+    c3 = None
     if D.world == 1 and D.rank == 0 and not args.no_single:
         try:
-            single = run_single(args)
+            c3 = run_config3(args)
         except Exception as e:  # reported, never silently replaced by another path
-            single = {"error": f"{type(e).__name__}: {e}"}
+            import traceback
+            traceback.print_exc()
+            c3 = {"error": f"{type(e).__name__}: {e}"}
 
     if D.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D.world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": sweep_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(fit, D.world, {"mode": "fast (FMA)" if args.fast else "exact (bitwise)",
-                                                  "schedule": "simple" if args.simple else "auto"}),
+            "config": config_block(fit.degrees, D.world, {"mode": "fast (FMA)" if args.fast else "exact (bitwise)",
+                                                          "schedule": "simple" if args.simple else "auto"}),
             "roofline": roof,
-            "sweep_roofline": {"bound": "hbm", "algorithmic_bytes_per_dof": ab["sweep"], "achieved": sweep_achieved,
-                               "peak": peak, "unit": "GB/s", "frac": sweep_achieved / peak},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "kernels": kernels, "clocks": clk,
+            "sweep_roofline": {"bound": roof_t["bound"], "algorithmic_bytes_per_dof": ab["sweep"],
+                               "algorithmic_fp64_ops_per_dof": ops,
+                               "achieved": ab["sweep"] * dofs_total / D.world / (sweep_ms / 1e3) / 1e9,
+                               "peak": roof_t["hbm_gbs"], "unit": "GB/s", "frac": t_roof / (sweep_ms / 1e3),
+                               "t_hbm_ms": roof_t["t_hbm_s"] * 1e3, "t_fp64_ms": roof_t["t_fp64_s"] * 1e3,
+                               "fp64_tflops_peak": roof_t["fp64_tflops"], "fp64_source": roof_t["fp64_source"]},
+            "cpu_baseline": cpu, "cpu_baseline_port": cpu_port, "e2e": e2e, "e2e_multi": e2e_multi,
+            "gpu_launches": launches, "kernels": kernels, "clocks": clk, "distributed": D.info(),
             "residual_norm2_last": float(norms[-1][-1]) if norms else None,
-            "single_tet": single,
+            "config3": c3,
         }
         print(json.dumps(line), flush=True)
 
@@ -483,18 +769,20 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--e2e-sweeps", type=int, default=3)
+    ap.add_argument("--e2e-sweeps", type=int, default=3, help="sweeps per host round trip of e2e_multi")
     ap.add_argument("--e2e-chunk", type=int, default=64, help="tets per pipelined host<->device chunk")
     ap.add_argument("--fast", action="store_true", help="FMA substitution (<=1e-12, not bitwise)")
     ap.add_argument("--simple", action="store_true", help="force the reference-layout kernels")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--no-single", action="store_true", help="skip the single-macro-tet (level 9) leg")
-    ap.add_argument("--single-level", type=int, default=9)
-    ap.add_argument("--single-sweeps", type=int, default=100)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline legs")
+    ap.add_argument("--no-single", action="store_true", help="skip the config-3 (level 9 single tet) leg")
+    ap.add_argument("--config3-sweeps", type=int, default=CFG3["sweeps"])
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup raised to 3 (timing rules)")
         args.warmup = 3
+    rc = relaunch_under_torchrun(args)
+    if rc is not None:
+        sys.exit(rc)
     # the reference arm runs on rank 0 only and needs no process group
     D = Dist("nccl", init=args.impl == "ours")
     try:

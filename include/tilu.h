@@ -67,6 +67,12 @@ typedef struct {
     const double *factors;      /* [grid][9] CellILU rows (ilu.py:210-227) for the stored-factor sweep,
                                    or NULL */
     int flags;                  /* TILU_FAST | TILU_SCHED_SIMPLE */
+    /* Separable scalar coefficient on the unit macro-tet (config 3), rows evaluated on the fly
+       instead of read (takes precedence over arow / arows_dev): HOST [3][4n+1] tables
+       c1*gx(c/4n), gy(c/4n), gz(c/4n); k = c0 + (hx*gy)*gz; W = n^2 |micro-tet| (stencil.py SeparableK).
+       NULL: not used. */
+    const double *sepk_tables;
+    double sepk_c0, sepk_w;
 } tilu_desc_t;
 
 /* Build a device plan: uploads coefficients, band rows and stencil, precomputes the
@@ -136,6 +142,11 @@ int tilu_stored_sweep(const tilu_plan_t *plan, double *u, const double *f, int n
 int64_t tilu_factorize_stream(int n, const int64_t *rowoff, const double *arows, int aconst,
                               double *full_store, int do_full, const int64_t *collect_ranks,
                               int64_t ncollect, double *collect_out, double pivot_eps);
+
+/* Host-side setup: rows [grid][15] (interior rows written, others untouched) of a separable scalar
+ * coefficient on the unit macro-tet from its [3][4n+1] tables -- bitwise the reference's per-point
+ * assembly stencil_source (assembly.py:208-221) for that coefficient.  HOST pointers. */
+int tilu_sepk_rows(int level, const double *tables, double c0, double w, double *rows);
 
 /* Introspection. */
 const char *tilu_last_error(void);

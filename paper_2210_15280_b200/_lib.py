@@ -35,7 +35,7 @@ class TiluDesc(ctypes.Structure):
         ("level", _I), ("kx1", _I), ("ky1", _I), ("kz1", _I), ("variant", _I),
         ("lcoefs", _P), ("dcoefs", _P), ("band_ranks", _P), ("nband", _L), ("store_rows", _P),
         ("arow", _P), ("arows_dev", _P), ("acoefs", _P), ("akx1", _I), ("aky1", _I), ("akz1", _I),
-        ("factors", _P), ("flags", _I),
+        ("factors", _P), ("flags", _I), ("sepk_tables", _P), ("sepk_c0", _D), ("sepk_w", _D),
     ]
 
 
@@ -47,7 +47,7 @@ EXPORTS = (
     "tilu_version", "tilu_last_launch_count", "tilu_plan_grid_size", "tilu_plan_interior_size",
     "tilu_profile_enable", "tilu_profile_reset", "tilu_profile_read", "tilu_packed_size",
     "tilu_packed_scratch_size", "tilu_pack",
-    "tilu_unpack", "tilu_sweep_packed", "tilu_plane_tasks",
+    "tilu_unpack", "tilu_sweep_packed", "tilu_plane_tasks", "tilu_sepk_rows",
 )
 
 
@@ -91,6 +91,8 @@ def lib():
         getattr(L, name).restype = _I
     L.tilu_sweep_packed.argtypes = [_P, _P, _P, _P, _I, _I, _P, _P]
     L.tilu_sweep_packed.restype = _I
+    L.tilu_sepk_rows.argtypes = [_I, _P, _D, _D, _P]
+    L.tilu_sepk_rows.restype = _I
     L.tilu_plane_tasks.argtypes = [_I, _P, _I]
     L.tilu_plane_tasks.restype = _I
     L.tilu_profile_enable.argtypes = [_I]

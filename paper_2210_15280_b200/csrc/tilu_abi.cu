@@ -150,7 +150,10 @@ static int plane_min_level()
 bool batch_ok(const tilu_plan_t *p)
 {
     // packed element offsets are 32-bit: grid * 64 < 2^32 (level <= 9)
-    return !(p->flags & TILU_SCHED_SIMPLE) && p->dev.level <= 9 && p->dev.n >= 4 && p->bsched != nullptr;
+    // the batched kernels compute the residual from the assembled stencil only: plans whose residual
+    // is the operator surrogate (seedA, a_mode='surrogate') take the reference-layout kernels
+    return !(p->flags & TILU_SCHED_SIMPLE) && p->dev.level <= 9 && p->dev.n >= 4 && p->bsched != nullptr &&
+           p->dev.seedA == nullptr && (p->dev.arow != nullptr || p->dev.arows != nullptr);
 }
 
 // Tets per lane of the packed layout (groups of 32 * tpl tets).  More tets per lane amortise the
@@ -164,15 +167,15 @@ int batch_tpl(int ntets)
     return ntets > 32 ? 2 : 1;
 }
 
-// Per-point coefficient tables (2 x [grid][8] doubles, shared by all tets of a batch) replace the
-// per-warp NDDF march for large batches: 46 MB at level 7 (L2-resident), 360 MB at level 8.  Built
-// on first use; TILU_TAB=0|1 overrides the choice (measurement only).
+// Per-point coefficient tables (2 x [grid][8] doubles, shared by all tets of a batch) can replace the
+// per-warp NDDF march for large batches: 46 MB at level 7 (L2-resident), 360 MB at level 8.  Off by
+// default -- the north star evaluates the L/U weights on the fly, and on config 4 the tables gain
+// only ~2% (r02a bench: 3.13 vs 3.19 ms/sweep).  TILU_TAB=1 turns them on (measurement only).
 static std::mutex g_coef_mu;
 static bool want_tables(const tilu_plan_t *p, int ntets)
 {
     static const char *e = std::getenv("TILU_TAB");
-    if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1' && p->dev.level <= 8;
-    return batch_tpl(ntets) == 2 && p->dev.level <= 8;
+    return e && e[0] == '1' && batch_tpl(ntets) == 2 && p->dev.level <= 8;
 }
 static int ensure_tables(const tilu_plan_t *cp, cudaStream_t s)
 {
@@ -446,14 +449,29 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
         tilu_plan_destroy(p);
         return rc;
     }
+    double *dsepk = nullptr;
+    if (d->sepk_tables) {
+        if (!(d->sepk_w > 0.0)) {
+            tilu_plan_destroy(p);
+            return fail(TILU_EINVAL, "separable coefficient: W must be positive");
+        }
+        if ((rc = dev_upload(p, &dsepk, d->sepk_tables, (size_t)3 * (4 * n + 1)))) {
+            tilu_plan_destroy(p);
+            return rc;
+        }
+        P.sepk = dsepk;
+        P.sepk_c0 = d->sepk_c0;
+        P.sepk_w = d->sepk_w;
+    }
     P.rows = drows;
     P.rowbase = drowbase;
     P.bandoff = dbandoff;
     P.store = dstore;
     P.seedF = dseedF;
     P.seedB = dseedB;
-    P.arow = darow;
-    P.arows = d->arow ? nullptr : d->arows_dev;
+    // one operator form: on-the-fly separable rows, else the constant row, else per-point rows
+    P.arow = dsepk ? nullptr : darow;
+    P.arows = (dsepk || d->arow) ? nullptr : d->arows_dev;
     P.factors = dfactors;
     if (d->acoefs) {
         P.akx1 = d->akx1;
@@ -524,12 +542,12 @@ static int residual_into(const tilu_plan_t *p, const double *u, const double *f,
         const bool ok = launch_residual_sop(P, u, f, w, part, ntets, s);
         prof_end("residual_sop", s);
         if (!ok) return fail(TILU_EUNSUPPORTED, "operator surrogate degree");
-    } else if (P.arow || P.arows) {
+    } else if (P.arow || P.arows || P.sepk) {
         prof_begin(s);
         launch_residual(P, !(p->flags & TILU_FAST), u, f, w, part, ntets, false, s);
         prof_end("residual", s);
     } else {
-        return fail(TILU_EINVAL, "plan has no operator (arow / arows_dev / acoefs)");
+        return fail(TILU_EINVAL, "plan has no operator (arow / arows_dev / acoefs / sepk_tables)");
     }
     ++g_launches;
     if (rnorm2) {
@@ -558,7 +576,7 @@ int tilu_stencil_apply(const tilu_plan_t *p, const double *u, double *out, int n
 {
     g_launches = 0;
     if (!valid_plan(p) || !u || !out || ntets < 1) return fail(TILU_EINVAL, "invalid arguments");
-    if (!p->dev.arow && !p->dev.arows) return fail(TILU_EINVAL, "plan has no stencil rows");
+    if (!p->dev.arow && !p->dev.arows && !p->dev.sepk) return fail(TILU_EINVAL, "plan has no stencil rows");
     launch_residual(p->dev, true, u, nullptr, out, nullptr, ntets, true, static_cast<cudaStream_t>(stream));
     g_launches = 1;
     return check_cuda("stencil_apply");

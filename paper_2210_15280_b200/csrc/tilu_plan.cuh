@@ -29,6 +29,8 @@ struct PlanDev {
     const double *seedB;             // [nrows][8][kx1]  backward pass: 7 shifted L + 1/D
     const double *arow;              // [15] constant stencil or nullptr
     const double *arows;             // [grid][15] per-point rows or nullptr
+    const double *sepk;              // [3][4n+1] separable-coefficient tables (rows on the fly) or nullptr
+    double sepk_c0, sepk_w;
     const double *seedA;             // [nrows][15][akx1] operator-surrogate tables or nullptr
     int akx1;
     const double *factors;           // [grid][9] stored ILU rows or nullptr

@@ -55,6 +55,7 @@
 
 #include "tilu_common.cuh"
 #include "tilu_plan.cuh"
+#include "tilu_sepk_dev.cuh"
 
 namespace tilu {
 void prof_begin(cudaStream_t s);
@@ -343,7 +344,9 @@ __device__ __forceinline__ void wait_armed(const double *hout, int t_first, int 
 // 15-point residual from TMA-staged planes) run ahead and pass their results through a
 // shared-memory ring of GS-step groups (mbarrier full / empty).
 // ------------------------------------------------------------------------------------------------
-template <int K, bool EXACT, bool CONST_ROW>
+// AMODE: 0 = per-point rows (P.arows), 1 = constant row (A.arow), 2 = separable coefficient rows
+// evaluated on the fly (P.sepk, config 3).
+template <int K, bool EXACT, int AMODE>
 __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, const Args A, const __grid_constant__ Maps M)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -560,6 +563,13 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
             // =========================== residual helper ========================================
             int64_t rbase = 0;
             if (live) rbase = P.rowbase[row_id(n, z, y)];
+            // separable coefficient: the y / z table windows are constant along the row
+            double gyw[7], gzw[7];
+            if (AMODE == 2) {
+                const int T4 = 4 * n + 1;
+                sepk_window(P.sepk + T4, live ? 4 * y : 4, gyw);
+                sepk_window(P.sepk + 2 * T4, live ? 4 * z : 4, gzw);
+            }
             auto issue = [&](int q) {  // lane 0: u box (planes s-1..s+1, lines tq-2 .. tq+GS+1) + f box
                 const int sl = tiss % NT;
                 const int tq = T0 + GS * q;
@@ -596,7 +606,11 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                     double res = 0.0;
                     if (sg >= lo && sg <= hi) {
                         double a[15];
-                        if (CONST_ROW) {
+                        if (AMODE == 2) {
+                            double hxw[7];
+                            sepk_window(P.sepk, 4 * (sg - z), hxw);
+                            sepk_row(hxw, gyw, gzw, P.sepk_c0, P.sepk_w, a);
+                        } else if (AMODE == 1) {
 #pragma unroll
                             for (int qq = 0; qq < 15; ++qq) a[qq] = A.arow[qq];
                         } else {
@@ -1056,42 +1070,44 @@ static std::vector<int> make_tasks(int n)
     return out;
 }
 
-template <int K, bool EXACT, bool CONST_ROW>
+template <int K, bool EXACT, int AMODE>
 static cudaError_t set_attrs()
 {
-    cudaError_t e = cudaFuncSetAttribute(k_plane_fwd<K, EXACT, CONST_ROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_plane_fwd<K, EXACT, AMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(Smem));
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_plane_bwd<K, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
 }
 
-template <int K, bool EXACT, bool CONST_ROW>
+template <int K, bool EXACT, int AMODE>
 static bool launch_k(const PlanDev &P, const Args &A, const Maps &M, int ctas, bool fwd, cudaStream_t s)
 {
-    static bool attrs = (set_attrs<K, EXACT, CONST_ROW>() == cudaSuccess);
+    static bool attrs = (set_attrs<K, EXACT, AMODE>() == cudaSuccess);
     if (!attrs) return false;
-    if (fwd) k_plane_fwd<K, EXACT, CONST_ROW><<<ctas, 3 * PW * 32, sizeof(Smem), s>>>(P, A, M);
+    if (fwd) k_plane_fwd<K, EXACT, AMODE><<<ctas, 3 * PW * 32, sizeof(Smem), s>>>(P, A, M);
     else k_plane_bwd<K, EXACT><<<ctas, 2 * PW * 32, sizeof(Smem), s>>>(P, A, M);
     return true;
 }
-template <bool EXACT, bool CONST_ROW>
+template <bool EXACT, int AMODE>
 static bool launch_e(const PlanDev &P, const Args &A, const Maps &M, int ctas, bool fwd, cudaStream_t s)
 {
     switch (P.kx1) {
-    case 1: return launch_k<1, EXACT, CONST_ROW>(P, A, M, ctas, fwd, s);
-    case 2: return launch_k<2, EXACT, CONST_ROW>(P, A, M, ctas, fwd, s);
-    case 3: return launch_k<3, EXACT, CONST_ROW>(P, A, M, ctas, fwd, s);
-    case 4: return launch_k<4, EXACT, CONST_ROW>(P, A, M, ctas, fwd, s);
-    case 5: return launch_k<5, EXACT, CONST_ROW>(P, A, M, ctas, fwd, s);
-    case 6: return launch_k<6, EXACT, CONST_ROW>(P, A, M, ctas, fwd, s);
+    case 1: return launch_k<1, EXACT, AMODE>(P, A, M, ctas, fwd, s);
+    case 2: return launch_k<2, EXACT, AMODE>(P, A, M, ctas, fwd, s);
+    case 3: return launch_k<3, EXACT, AMODE>(P, A, M, ctas, fwd, s);
+    case 4: return launch_k<4, EXACT, AMODE>(P, A, M, ctas, fwd, s);
+    case 5: return launch_k<5, EXACT, AMODE>(P, A, M, ctas, fwd, s);
+    case 6: return launch_k<6, EXACT, AMODE>(P, A, M, ctas, fwd, s);
     default: return false;
     }
 }
 static bool launch_pass(const PlanDev &P, const Args &A, const Maps &M, int ctas, bool exact, bool fwd, cudaStream_t s)
 {
-    const bool c = P.arow != nullptr;
-    if (exact) return c ? launch_e<true, true>(P, A, M, ctas, fwd, s) : launch_e<true, false>(P, A, M, ctas, fwd, s);
-    return c ? launch_e<false, true>(P, A, M, ctas, fwd, s) : launch_e<false, false>(P, A, M, ctas, fwd, s);
+    const int am = P.sepk ? 2 : P.arow ? 1 : 0;
+    if (exact) return am == 2 ? launch_e<true, 2>(P, A, M, ctas, fwd, s)
+                    : am == 1 ? launch_e<true, 1>(P, A, M, ctas, fwd, s) : launch_e<true, 0>(P, A, M, ctas, fwd, s);
+    return am == 2 ? launch_e<false, 2>(P, A, M, ctas, fwd, s)
+         : am == 1 ? launch_e<false, 1>(P, A, M, ctas, fwd, s) : launch_e<false, 0>(P, A, M, ctas, fwd, s);
 }
 
 static int resident_ctas(const tilu_plan *p)
@@ -1168,7 +1184,7 @@ bool plane_supported(const tilu_plan *p)
     static const char *e = std::getenv("TILU_PLANE");
     if (e && e[0] == '0') return false;
     return p->dev.kx1 <= 6 && p->dev.level >= 3 && p->dev.level <= 10 && p->dev.seedA == nullptr &&
-           (p->dev.arow != nullptr || p->dev.arows != nullptr);
+           (p->dev.arow != nullptr || p->dev.arows != nullptr || p->dev.sepk != nullptr);
 }
 
 void plane_free(void *ws)

@@ -11,6 +11,7 @@
 // fallback for shapes the plane-layout fast path does not cover.
 #include "tilu_common.cuh"
 #include "tilu_plan.cuh"
+#include "tilu_sepk_dev.cuh"
 
 namespace tilu {
 
@@ -72,7 +73,8 @@ __global__ void k_seed_op(PlanDev P, const double *__restrict__ acoefs, int ky1,
 // w[interior] = f - out as in multigrid.py:420-427).  One CTA per (row, tet); per-row sum of
 // squares into part[tet][row] for a deterministic norm.
 // ----------------------------------------------------------------------------------------------
-template <bool EXACT, bool CONST_ROW, bool APPLY_ONLY>
+// AMODE: 0 = per-point rows, 1 = constant row, 2 = separable coefficient rows evaluated on the fly.
+template <bool EXACT, int AMODE, bool APPLY_ONLY>
 __global__ void __launch_bounds__(128) k_residual(PlanDev P, const double *__restrict__ uall,
                                                   const double *__restrict__ fall, double *__restrict__ wall,
                                                   double *__restrict__ part)
@@ -91,7 +93,9 @@ __global__ void __launch_bounds__(128) k_residual(PlanDev P, const double *__res
     double ss = 0.0;
     for (int x = 1 + threadIdx.x; x <= ri.xe; x += blockDim.x) {
         const int64_t p = base + x;
-        const double *a = CONST_ROW ? P.arow : P.arows + 15 * p;
+        double sa[15];
+        if (AMODE == 2) sepk_point(P, x, y, z, sa);
+        const double *a = AMODE == 2 ? sa : AMODE == 1 ? P.arow : P.arows + 15 * p;
         double acc = EXACT ? dmul(a[7], u[p]) : a[7] * u[p];
         acc = madd<EXACT>(acc, a[0], u[p - 1]);
         acc = madd<EXACT>(acc, a[1], u[rs + x]);
@@ -358,19 +362,22 @@ void launch_residual(const PlanDev &P, bool exact, const double *u, const double
                      int ntets, bool apply_only, cudaStream_t s)
 {
     dim3 grid(P.nrows, ntets);
-    const bool c = P.arow != nullptr;
+    const int am = P.sepk ? 2 : P.arow ? 1 : 0;
+#define TILU_RES(E, M, A) k_residual<E, M, A><<<grid, 128, 0, s>>>(P, u, f, w, A ? nullptr : part)
     if (apply_only) {
-        if (c) k_residual<true, true, true><<<grid, 128, 0, s>>>(P, u, f, w, nullptr);
-        else k_residual<true, false, true><<<grid, 128, 0, s>>>(P, u, f, w, nullptr);
-        return;
-    }
-    if (exact) {
-        if (c) k_residual<true, true, false><<<grid, 128, 0, s>>>(P, u, f, w, part);
-        else k_residual<true, false, false><<<grid, 128, 0, s>>>(P, u, f, w, part);
+        if (am == 2) TILU_RES(true, 2, true);
+        else if (am == 1) TILU_RES(true, 1, true);
+        else TILU_RES(true, 0, true);
+    } else if (exact) {
+        if (am == 2) TILU_RES(true, 2, false);
+        else if (am == 1) TILU_RES(true, 1, false);
+        else TILU_RES(true, 0, false);
     } else {
-        if (c) k_residual<false, true, false><<<grid, 128, 0, s>>>(P, u, f, w, part);
-        else k_residual<false, false, false><<<grid, 128, 0, s>>>(P, u, f, w, part);
+        if (am == 2) TILU_RES(false, 2, false);
+        else if (am == 1) TILU_RES(false, 1, false);
+        else TILU_RES(false, 0, false);
     }
+#undef TILU_RES
 }
 
 template <int K>

@@ -49,15 +49,31 @@ def _as_batch(t, grid: int, name: str):
     return t, (1 if t.dim() == 1 else t.shape[0])
 
 
+def _same_batch(ref, T: int, grid: int, **others):
+    """Every tensor in ``others`` must be a CUDA fp64 batch of exactly ``ref``'s shape on ``ref``'s
+    device: the kernels read ``T * grid`` doubles from each of them."""
+    out = []
+    for name, t in others.items():
+        t, Tn = _as_batch(t, grid, name)
+        if tuple(t.shape) != tuple(ref.shape) or Tn != T:
+            raise ValueError(f"{name}: shape {tuple(t.shape)} does not match u's {tuple(ref.shape)}")
+        if t.device != ref.device:
+            raise ValueError(f"{name}: on {t.device}, u on {ref.device}")
+        out.append(t)
+    return out
+
+
 class DevicePlan:
     """Owner of one ``tilu_plan_t`` (coefficients, band rows, operator and seed tables on device)."""
 
     def __init__(self, level: int, lcoefs, dcoefs, variant: str = "v1", band_ranks=None, store_rows=None,
                  arow=None, arows=None, acoefs=None, factors=None, fast: bool = False, simple: bool = False,
-                 schedule: str = "auto"):
+                 schedule: str = "auto", sepk=None):
         """schedule: "auto" (single tets: plane kernels from level 5, batches: interleaved kernels),
         "simple" (reference-layout wavefront kernels), "plane" (plane kernels at every level),
-        "batch" (interleaved dataflow kernels for single tets too)."""
+        "batch" (interleaved dataflow kernels for single tets too).
+        sepk: a stencil.SeparableK -- the residual evaluates the separable coefficient's rows on the
+        fly (config 3) instead of reading arow / arows."""
         L = _lib.lib()
         self.level = int(level)
         self.variant = variant
@@ -87,6 +103,13 @@ class DevicePlan:
             d.akx1, d.aky1, d.akz1 = ac.shape[1:]
         if factors is not None:
             d.factors = self._ptr(_f64(factors))
+        if sepk is not None:
+            if int(sepk.level) != self.level:
+                raise ValueError(f"sepk tables are for level {sepk.level}, plan level {self.level}")
+            tab = _f64(sepk.tables)
+            if tab.shape != (3, 4 * 2 ** self.level + 1):
+                raise ValueError("sepk tables must be [3, 4n+1]")
+            d.sepk_tables, d.sepk_c0, d.sepk_w = self._ptr(tab), float(sepk.c0), float(sepk.w)
         if schedule not in ("auto", "simple", "plane", "batch"):
             raise ValueError(f"unknown schedule {schedule!r}")
         simple = simple or schedule == "simple"
@@ -134,10 +157,9 @@ class DevicePlan:
 
     def residual(self, u, f, w=None, norms: bool = False):
         u, T = _as_batch(u, self.grid, "u")
-        f, _ = _as_batch(f, self.grid, "f")
         if w is None:
             w = torch.zeros_like(u)
-        w, _ = _as_batch(w, self.grid, "w")
+        f, w = _same_batch(u, T, self.grid, f=f, w=w)
         rn = torch.empty(T, dtype=torch.float64, device=u.device) if norms else None
         _lib.check(_lib.lib().tilu_residual(self._h, u.data_ptr(), f.data_ptr(), w.data_ptr(), T,
                                             None if rn is None else rn.data_ptr(), _stream_ptr()))
@@ -147,6 +169,7 @@ class DevicePlan:
         u, T = _as_batch(u, self.grid, "u")
         if out is None:
             out = torch.zeros_like(u)
+        (out,) = _same_batch(u, T, self.grid, out=out)
         _lib.check(_lib.lib().tilu_stencil_apply(self._h, u.data_ptr(), out.data_ptr(), T, _stream_ptr()))
         return out
 
@@ -154,7 +177,7 @@ class DevicePlan:
         """``sweeps`` smoothing steps in place on u; returns ||f - A u||^2 before each sweep
         ([sweeps, ntets]) when ``norms``."""
         u, T = _as_batch(u, self.grid, "u")
-        f, _ = _as_batch(f, self.grid, "f")
+        (f,) = _same_batch(u, T, self.grid, f=f)
         rn = torch.empty((sweeps, T), dtype=torch.float64, device=u.device) if norms else None
         fn = _lib.lib().tilu_stored_sweep if stored else _lib.lib().tilu_sweep
         _lib.check(fn(self._h, u.data_ptr(), f.data_ptr(), T, int(sweeps),
@@ -175,7 +198,10 @@ class DevicePlan:
 
     def pack(self, src, ntets: int | None = None, out=None):
         src, T = _as_batch(src, self.grid, "src")
-        T = T if ntets is None else ntets
+        if ntets is not None:
+            if not 1 <= int(ntets) <= T:
+                raise ValueError(f"ntets={ntets}: src holds {T} tets")
+            T = int(ntets)
         if out is None:
             out = torch.empty(self.packed_numel(T), dtype=torch.float64, device=src.device)
         _lib.check(_lib.lib().tilu_pack(self._h, src.data_ptr(), out.data_ptr(), T, _stream_ptr()))
@@ -322,8 +348,12 @@ class SurrogateILUSmoother:
         self.config = config
         self.grid = lattice.grid_size(level)
         op = {}
-        if config.a_mode == "surrogate":
+        # the operator surrogate replaces the assembled residual only for the surrogate smoother
+        # (reference multigrid.py:418: use_surrogate_a = a_mode == 'surrogate' and kind == 'surrogate_ilu')
+        if config.a_mode == "surrogate" and config.kind == "surrogate_ilu":
             op["acoefs"] = fitting.fit_surrogate_operator(source, level, config.a_degrees, config.sample_level)
+        elif source.sepk is not None:
+            op["sepk"] = source.sepk          # rows evaluated on the fly: nothing per point uploaded
         elif source.constant:
             op["arow"] = np.atleast_1d(source.data)
         else:

@@ -122,6 +122,29 @@ def micro_positions(vertices: np.ndarray, level: int) -> np.ndarray:
 
 
 @dataclass
+class SeparableK:
+    """Table form of a separable scalar coefficient's rows on the unit macro-tet: k at a centroid
+    (4p + a) / (4n) is c0 + (tables[0][4x+ax] * tables[1][4y+ay]) * tables[2][4z+az]; the rows
+    follow from separable_program (compiled into csrc/tilu_sepk.h).  W = n^2 |T|."""
+
+    level: int
+    tables: np.ndarray   # [3][4n+1]
+    c0: float
+    w: float
+
+    def rows(self) -> np.ndarray:
+        """[grid][15] rows (interior filled, zero elsewhere) from the native builder."""
+        import ctypes
+
+        from . import _lib
+        out = np.zeros((lattice.grid_size(self.level), 15))
+        tab = np.ascontiguousarray(self.tables, dtype=np.float64)
+        _lib.check(_lib.lib().tilu_sepk_rows(self.level, tab.ctypes.data, ctypes.c_double(self.c0),
+                                             ctypes.c_double(self.w), out.ctypes.data))
+        return out
+
+
+@dataclass
 class StencilSource:
     """Operator rows of one refined macro-tet: ``data`` is one row (constant) or
     [grid_size, 15] with only interior rows filled (reference assembly.py:173-194)."""
@@ -129,6 +152,7 @@ class StencilSource:
     level: int
     data: np.ndarray
     constant: bool
+    sepk: "SeparableK | None" = None   # table form of the rows (separable coefficient, unit tet)
 
     @property
     def kernel_args(self) -> tuple[np.ndarray, bool]:
@@ -145,9 +169,20 @@ def _deep_point(level: int) -> np.ndarray:
     return np.array((q, q, q), dtype=np.int64)
 
 
-def stencil_source(vertices, level: int, coeff: CoefficientField) -> StencilSource:
-    """Assemble the 15-point rows of the P1 operator -div(K grad u) on a refined macro-tet."""
+def stencil_source(vertices, level: int, coeff: CoefficientField, *, native: bool = True) -> StencilSource:
+    """Assemble the 15-point rows of the P1 operator -div(K grad u) on a refined macro-tet.
+
+    A separable scalar coefficient on the unit macro-tet (config 3) is assembled by the native
+    row builder (``tilu_sepk_rows``: the same rows bitwise, in seconds instead of the numpy path's
+    ~30 min at level 9), and the source keeps the table form (``sepk``) so the GPU residual can
+    evaluate the rows on the fly instead of reading them; ``native=False`` forces the numpy path."""
     vertices = np.asarray(getattr(vertices, "vertices", vertices), dtype=np.float64)
+    if isinstance(coeff, SeparableScalar) and separable_program(vertices, level) is not None:
+        sk = SeparableK(level, coeff.tables(level), coeff.c0, separable_program(vertices, level)[1])
+        if native:
+            return StencilSource(level, sk.rows(), False, sk)
+        src = stencil_source(vertices, level, CoefficientField.scalar(coeff.fn, coeff.name), native=False)
+        return StencilSource(level, src.data, False, sk)
     pos = micro_positions(vertices, level)
     if coeff.is_constant:
         p = _deep_point(level)
@@ -171,12 +206,81 @@ def stencil_source(vertices, level: int, coeff: CoefficientField) -> StencilSour
     return StencilSource(level, data, False)
 
 
-def sin_kappa() -> CoefficientField:
+class SeparableScalar(CoefficientField):
+    """Scalar coefficient k(x, y, z) = c0 + c1 * gx(x) * gy(y) * gz(z), evaluated left to right in
+    exactly that order (so its values are bitwise those of the same Python expression).  Besides
+    the generic per-point assembly, a separable field on the unit macro-tet has a table form
+    (``tables``) that the native row builder and the GPU residual evaluate on the fly."""
+
+    def __init__(self, gx, gy, gz, c0: float = 0.0, c1: float = 1.0, name: str = "separable"):
+        self.gx, self.gy, self.gz = gx, gy, gz
+        self.c0, self.c1 = float(c0), float(c1)
+
+        def fn(p):
+            p = np.atleast_2d(p)
+            return self.c0 + self.c1 * gx(p[:, 0]) * gy(p[:, 1]) * gz(p[:, 2])
+        super().__init__(fn=lambda pts: np.asarray(fn(pts), dtype=np.float64), name=name)
+
+    def tables(self, level: int) -> np.ndarray:
+        """[3][4n+1]: c1*gx, gy, gz at the abscissae c / (4n), c = 0..4n -- every coordinate a
+        micro-element centroid of the unit macro-tet can take (the mean of four lattice points)."""
+        n = 2 ** level
+        t = np.arange(4 * n + 1, dtype=np.float64) / (4.0 * n)
+        return np.ascontiguousarray(np.stack([self.c1 * self.gx(t), self.gy(t), self.gz(t)]), dtype=np.float64)
+
+
+def _sin2pi(t):
+    return np.sin(2 * np.pi * t)
+
+
+def sin_kappa() -> SeparableScalar:
     """Config 3's coefficient k(x) = 1 + 0.5 sin(2 pi x) sin(2 pi y) sin(2 pi z)."""
-    def fn(p):
-        p = np.atleast_2d(p)
-        return 1.0 + 0.5 * np.sin(2 * np.pi * p[:, 0]) * np.sin(2 * np.pi * p[:, 1]) * np.sin(2 * np.pi * p[:, 2])
-    return CoefficientField.scalar(fn, name="sin_kappa")
+    return SeparableScalar(_sin2pi, _sin2pi, _sin2pi, c0=1.0, c1=0.5, name="sin_kappa")
+
+
+# ------------------------------------------------------------------------------------------
+# on-the-fly rows of a separable scalar coefficient on the unit macro-tet
+# ------------------------------------------------------------------------------------------
+
+def separable_program(vertices, level: int):
+    """The per-point rows of a scalar coefficient as a fixed program, or None if the macro-tet does
+    not admit it.
+
+    On the unit macro-tet every micro-element has gradients in {0, +-n} and the same volume, so
+    element_matrices' einsum (path: K contracted with grads, then with grads, then the volume)
+    reduces, for K = k I, to  S[li, j] = fl(fl(m k) W)  with the integer m = sum_e g_li,e g_j,e / n^2
+    in {-2..3} and W = n^2 |T| (exact power-of-two scaling), and the element's centroid is exactly
+    (4p + a) / (4n) for a small integer offset a.  Row entry d of point p is the sum of those
+    contributions over the 24 elements of VERTEX_PATCH in patch order (zero contributions dropped:
+    adding +-0 to the +0-initialised accumulator is the identity).
+    Returns (elements, W): elements[e] = ((ax, ay, az), [(direction, m), ...]) in patch order."""
+    vertices = np.asarray(getattr(vertices, "vertices", vertices), dtype=np.float64)
+    if not np.array_equal(vertices, lattice.unit_tet()):
+        return None
+    n = 2 ** level
+    pos = micro_positions(vertices, level)
+    p = _deep_point(level)
+    elements, vols = [], set()
+    for ci, li, rel, dirs in VERTEX_PATCH:
+        verts = pos[lattice.lattice_rank(p + rel, level)][None]
+        E = verts[:, 1:] - verts[:, :1]
+        det = np.linalg.det(E)
+        g = np.empty((1, 4, 3))
+        g[:, 1:] = np.linalg.inv(E).transpose(0, 2, 1)
+        g[:, 0] = -g[:, 1:].sum(axis=1)
+        g = g[0] / n
+        if not np.all(np.isin(g, (-1.0, 0.0, 1.0))):
+            return None
+        vols.add(float(np.abs(det[0]) / 6.0))
+        contrib = []
+        for j in range(4):
+            m = int(sum(g[li, e] * g[j, e] for e in range(3)))
+            if m != 0:
+                contrib.append((int(dirs[j]), m))
+        elements.append((tuple(int(v) for v in rel.sum(axis=0)), contrib))
+    if len(vols) != 1:
+        return None
+    return elements, vols.pop() * float(n) ** 2
 
 
 def diag_tensor(diag) -> CoefficientField:

@@ -1,0 +1,77 @@
+"""API guards and routing on the GPU (advisor findings, round 1):
+* operator-surrogate plans (a_mode='surrogate') at level >= 6 and for batches must not reach the
+  batched kernels (they have no surrogate residual) -- they run and match the oracle;
+* kind='ilu' uses the assembled operator even when a_mode='surrogate' (reference multigrid.py:418);
+* mismatched batch shapes / devices raise instead of reading past an allocation."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from paper_2210_15280_b200 import DevicePlan, SurrogateILUSmoother, lattice  # noqa: E402
+from paper_2210_15280_b200 import fitting as F  # noqa: E402
+from paper_2210_15280_b200 import stencil as S  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def cuda(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+
+
+def u0_of(level, ntets=1, seed=0):
+    mask = lattice.interior_mask(level)
+    rng = np.random.default_rng(seed)
+    u = np.zeros((ntets, lattice.grid_size(level)))
+    for t in range(ntets):
+        u[t, mask] = rng.uniform(-1, 1, int(mask.sum()))
+    return u
+
+
+@pytest.mark.parametrize("level,ntets", [(6, 1), (4, 2), (5, 3)])
+def test_operator_surrogate_plan_routes_safely(level, ntets):
+    src = S.stencil_source(lattice.unit_tet(), level, S.sin_kappa())
+    fit = F.fit_surrogate_ilu(src, level, (4, 4, 4), "v1")
+    ac = F.fit_surrogate_operator(src, level, (3, 3, 3))
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, acoefs=ac)
+    u0 = u0_of(level, ntets)
+    f = np.zeros_like(u0)
+    u = cuda(u0)
+    p.sweep(u, cuda(f), 2)
+    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows)
+    for t in range(ntets):
+        ref = u0[t].copy()
+        O.sweeps(sur, level, None, ref, f[t], 2, acoefs=ac)
+        assert np.array_equal(u[t].cpu().numpy(), ref)
+
+
+def test_ilu_kind_ignores_operator_surrogate():
+    level = 5
+    cfg = dict(kind="ilu", a_mode="surrogate", a_degrees=(2, 2, 2))
+    sm = SurrogateILUSmoother.setup(lattice.unit_tet(), level, (4, 4, 4), coeff=S.sin_kappa(), **cfg)
+    assert sm.plan is not None
+    u0 = u0_of(level)[0]
+    f = np.zeros_like(u0)
+    u = cuda(u0)
+    sm.apply(u, cuda(f), 2)
+    ref = u0.copy()
+    O.sweeps(None, level, sm.source.data, ref, f, 2, factors=sm.factorization.rows)
+    assert np.array_equal(u.cpu().numpy(), ref)
+
+
+def test_batch_shape_mismatch_raises():
+    level = 4
+    src = S.stencil_source(lattice.unit_tet(), level, S.CoefficientField.constant(1.0))
+    fit = F.fit_surrogate_ilu(src, level, (3, 3, 3), "v1")
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data)
+    g = lattice.grid_size(level)
+    u2 = torch.zeros((2, g), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        p.sweep(u2, torch.zeros(g, dtype=torch.float64, device="cuda"), 1)
+    with pytest.raises(ValueError):
+        p.residual(u2, torch.zeros((3, g), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        p.pack(u2, ntets=3)
+    with pytest.raises(ValueError):
+        p.stencil_apply(u2, out=torch.zeros((1, g), dtype=torch.float64, device="cuda"))
