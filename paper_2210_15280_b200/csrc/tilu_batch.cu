@@ -59,21 +59,34 @@ __device__ __forceinline__ Vt<T> ldv(const double *p)
     }
     return r;
 }
+// Load of w values produced concurrently by other warps (possibly still the sentinel): relaxed,
+// GPU scope (tilu_common.cuh ld_rlx).
 template <int T>
 __device__ __forceinline__ Vt<T> ldcgv(const double *p)
 {
     Vt<T> r;
     if constexpr (T == 1) {
-        r.a[0] = __ldcg(p);
+        r.a[0] = ld_rlx(p);
     } else {
 #pragma unroll
         for (int i = 0; i < T / 2; ++i) {
-            const double2 d = __ldcg(reinterpret_cast<const double2 *>(p) + i);
+            const double2 d = ld_rlx2(p + 2 * i);
             r.a[2 * i] = d.x;
             r.a[2 * i + 1] = d.y;
         }
     }
     return r;
+}
+// Store of a w value other warps poll for: relaxed, GPU scope.
+template <int T>
+__device__ __forceinline__ void st_hand(double *p, const Vt<T> &v)
+{
+    if constexpr (T == 1) {
+        st_rlx(p, v.a[0]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) st_rlx2(p + 2 * i, v.a[2 * i], v.a[2 * i + 1]);
+    }
 }
 template <int T>
 __device__ __forceinline__ void stv(double *p, const Vt<T> &v)
@@ -146,11 +159,11 @@ __device__ __forceinline__ void st_sent(double *p, uint64_t pol)
 {
     const double sv = __longlong_as_double(kSent);
     if constexpr (T == 1) {
-        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(sv), "l"(pol) : "memory");
+        asm volatile("st.relaxed.gpu.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(sv), "l"(pol) : "memory");
     } else {
 #pragma unroll
         for (int i = 0; i < T / 2; ++i)
-            asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p + 2 * i), "d"(sv), "d"(sv), "l"(pol)
+            asm volatile("st.relaxed.gpu.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p + 2 * i), "d"(sv), "d"(sv), "l"(pol)
                          : "memory");
     }
 }
@@ -518,7 +531,7 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
                 }
                 v.a[t] = vv;
             }
-            stv<T>(wa + R.oc + X, v);
+            st_hand<T>(wa + R.oc + X, v);
             st_sent<T>(wb + R.oc + X, pol_ef);  // re-arm w_b for the backward pass
             if constexpr (!TAB) smem_march<7, K>(tab, lane);
             if (slot == PC - 1 || x == m) {  // chunk consumed by every lane: refill its stage
@@ -751,7 +764,7 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
                 v.a[t] = vv;
                 un.a[t] = dadd(uo.a[t], vv);
             }
-            stv<T>(wb + R.oc + X, v);
+            st_hand<T>(wb + R.oc + X, v);
             stv<T>(u + R.oc + X, un);
             st_sent<T>(wa + R.oc + X, pol_ef);  // re-arm w_f for the next forward pass
             if constexpr (!TAB) smem_march<8, K>(tab, lane);

@@ -26,6 +26,33 @@ __device__ __forceinline__ double madd(double acc, double a, double b)
     return fma(a, b, acc);
 }
 
+// Handoff accesses of the data-is-the-flag protocol (a value produced by another warp / CTA during
+// the same kernel, polled until it is no longer the sentinel): morally strong relaxed accesses at
+// GPU scope -- single-copy atomic and eventually visible under the PTX memory model -- issued as
+// asm volatile so the compiler never caches a polled value in a register or drops / merges a
+// store.  They compile to the same LDG/STG.E.STRONG.GPU as ld.global.cg / a plain store (the L1
+// is bypassed either way); no ordering with other addresses is needed (each value is its own flag).
+__device__ __forceinline__ double ld_rlx(const double *p)
+{
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ld_rlx2(const double *p)
+{
+    double2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_rlx(double *p, double v)
+{
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v));
+}
+__device__ __forceinline__ void st_rlx2(double *p, double a, double b)
+{
+    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b));
+}
+
 __host__ __device__ __forceinline__ int64_t num_points(int64_t m)
 {
     return m < 0 ? 0 : (m + 1) * (m + 2) * (m + 3) / 6;

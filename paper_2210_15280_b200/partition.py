@@ -53,6 +53,38 @@ def allreduce_norms(local: "torch.Tensor", group=None) -> "torch.Tensor":
     return local
 
 
+class SweepNorms:
+    """Per-sweep global residual norm^2 of a macro-mesh: each rank adds its tets' ||r||^2 (fixed
+    order: groups in order, tets in order within a group's per-tet vector), then one allreduce per
+    sweep.  On CUDA tensors the allreduce of sweep k is enqueued on a side stream that waits only
+    for sweep k, so it overlaps sweep k+1; on CPU tensors (gloo) it runs inline."""
+
+    def __init__(self, sweeps: int, device, group=None):
+        self.norms = torch.zeros(sweeps, dtype=torch.float64, device=device)
+        self.group = group
+        self.side = None
+        if self.norms.is_cuda:
+            self.side = torch.cuda.Stream(device=self.norms.device)
+
+    def add(self, k: int, per_tet: "torch.Tensor") -> None:
+        self.norms[k] += per_tet.sum()
+
+    def close_sweep(self, k: int) -> None:
+        if self.side is None:
+            allreduce_norms(self.norms[k:k + 1], self.group)
+            return
+        ev = torch.cuda.Event()
+        ev.record()
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(ev)
+            allreduce_norms(self.norms[k:k + 1], self.group)
+
+    def result(self) -> "torch.Tensor":
+        if self.side is not None:
+            torch.cuda.current_stream(self.norms.device).wait_stream(self.side)
+        return self.norms
+
+
 class MacroMeshSmoother:
     """Smoother over this rank's share of a macro-mesh of independent macro-tets."""
 
@@ -69,7 +101,7 @@ class MacroMeshSmoother:
         self.groups = group_by_operator([s.data for s in sources])
         self.smoothers = [SurrogateILUSmoother(sources[g[0]], level, SmootherConfig(
             "surrogate_ilu", tuple(degrees), variant), fast=fast, simple=simple) for g in self.groups]
-        self._side = None
+        self._agg = None
         self.launches = 0   # kernels enqueued by apply() so far (bench accounting)
 
     @property
@@ -81,9 +113,7 @@ class MacroMeshSmoother:
         ||f - A u||^2 before each sweep ([sweeps], summed over all ranks) if requested."""
         if u.shape != (self.ntets_local, self.grid):
             raise ValueError(f"u must be [{self.ntets_local}, {self.grid}]")
-        norms = torch.zeros(sweeps, dtype=torch.float64, device=u.device) if residual_norms else None
-        if self._side is None and residual_norms:
-            self._side = torch.cuda.Stream(device=u.device)
+        agg = SweepNorms(sweeps, u.device, self.group) if residual_norms else None
         views = []
         for g, sm in zip(self.groups, self.smoothers):
             contiguous = g == list(range(g[0], g[0] + len(g)))
@@ -99,18 +129,11 @@ class MacroMeshSmoother:
                     rn = sm.apply(ug, f.index_select(0, idx).contiguous(), 1, residual_norms=residual_norms)
                     u.index_copy_(0, idx, ug)
                 self.launches += sm.plan.last_launch_count()
-                if residual_norms:
-                    norms[k] += rn.sum()
-            if residual_norms:
-                # overlap the collective with the next sweep: side stream waits for this sweep only
-                ev = torch.cuda.Event()
-                ev.record()
-                with torch.cuda.stream(self._side):
-                    self._side.wait_event(ev)
-                    allreduce_norms(norms[k:k + 1], self.group)
-        if residual_norms:
-            torch.cuda.current_stream().wait_stream(self._side)
-        return norms
+                if agg is not None:
+                    agg.add(k, rn)
+            if agg is not None:
+                agg.close_sweep(k)   # overlaps the next sweep (side stream)
+        return agg.result() if agg is not None else None
 
     # -- resident packed state (the hot path of the benchmark) ----------------------------------
     def load(self, u: "torch.Tensor", f: "torch.Tensor") -> None:
@@ -128,24 +151,20 @@ class MacroMeshSmoother:
         """``sweeps`` fused sweeps on the resident packed state; per-sweep global ||r||^2 is
         allreduced on a side stream (overlapping the next sweep)."""
         dev = self._res[0][2].device
-        norms = torch.zeros(sweeps, dtype=torch.float64, device=dev) if residual_norms else None
-        if residual_norms and self._side is None:
-            self._side = torch.cuda.Stream(device=dev)
+        if residual_norms and (self._agg is None or len(self._agg.norms) != sweeps):
+            self._agg = SweepNorms(sweeps, dev, self.group)
+        agg = self._agg if residual_norms else None
+        if agg is not None:
+            agg.norms = torch.zeros(sweeps, dtype=torch.float64, device=dev)
         for k in range(sweeps):
             for sm, g, up, fp, wp in self._res:
                 rn = sm.plan.sweep_packed(up, fp, wp, len(g), 1, norms=residual_norms)
                 self.launches += sm.plan.last_launch_count()
-                if residual_norms:
-                    norms[k] += rn.sum()
-            if residual_norms:
-                ev = torch.cuda.Event()
-                ev.record()
-                with torch.cuda.stream(self._side):
-                    self._side.wait_event(ev)
-                    allreduce_norms(norms[k:k + 1], self.group)
-        if residual_norms:
-            torch.cuda.current_stream().wait_stream(self._side)
-        return norms
+                if agg is not None:
+                    agg.add(k, rn)
+            if agg is not None:
+                agg.close_sweep(k)
+        return agg.result() if agg is not None else None
 
     def store(self, u: "torch.Tensor") -> "torch.Tensor":
         """Unpack the resident state back into u [ntets_local, grid] (reference layout)."""

@@ -9,7 +9,7 @@ rows), q = 6 -> build_surrogate_ilu with single-threaded BLAS.  Inputs as BASELI
 f ~ N(0, 1) (numpy default_rng(3), interior rank order), u = 0, 100 sweeps.  The C oracle
 (oracle/tilu_oracle.c, the reference kernels' bitwise restatement) runs the sweeps.
 
-Stored (tests/golden/cfg3_L9.npz, small): the fitted arrays (lcoefs, dcoefs; the LSQ depends on the
+Stored (tests/golden/l9_config3.npz, small): the fitted arrays (lcoefs, dcoefs; the LSQ depends on the
 host BLAS, so the GPU test uses these instead of refitting), the coefficient tables, W, SHA-256 of
 the band rows (recomputed by the deterministic native factorization on the GPU box and checked),
 the per-sweep residual norms ||f - A u_k||^2 (k = 0..99, before each sweep) and after the last sweep,
@@ -34,7 +34,7 @@ from paper_2210_15280_b200 import fitting, lattice, stencil  # noqa: E402
 
 LEVEL, Q, SWEEPS, FSEED, STEP = 9, 6, 100, 3, 1999
 SNAP = (1, 2, 3, 100)
-OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cfg3_L9.npz")
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "l9_config3.npz")
 
 
 def sha(a: np.ndarray) -> str:

@@ -2,7 +2,7 @@
 operator rows evaluated on the fly from the separable tables (stencil.SeparableK): no per-point rows
 on the device.  Bar: bitwise vs the C oracle fed the reference-equal per-point rows (exact mode),
 <= 1e-12 per sweep in fast (FMA) mode; at level 9 (the north star's size) against the committed
-oracle fixture tests/golden/cfg3_L9.npz (SHA-256 of the full u after sweeps 1, 2, 3, 100)."""
+oracle fixture tests/golden/l9_config3.npz (SHA-256 of the full u after sweeps 1, 2, 3, 100)."""
 import hashlib
 import os
 
@@ -111,9 +111,9 @@ def _sha(a):
 
 @pytest.fixture(scope="module")
 def l9():
-    path = os.path.join(GOLDEN, "cfg3_L9.npz")
+    path = os.path.join(GOLDEN, "l9_config3.npz")
     if not os.path.exists(path):
-        pytest.skip("cfg3_L9.npz not generated (tests/golden/make_config3_l9.py)")
+        pytest.skip("l9_config3.npz not generated (tests/golden/make_config3_l9.py)")
     g = np.load(path)
     level = int(g["level"])
     sk = S.SeparableK(level, g["tables"], float(g["c0"]), float(g["w"]))

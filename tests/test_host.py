@@ -122,3 +122,57 @@ def test_allreduce_norms_gloo_world2():
     total = 384 * 385 / 2
     assert out[0][1] == total and out[1][1] == total
     assert out[0][2] == [0] and out[1][2] == [192]
+
+
+def _sweepnorms_worker(rank, world, port, q):
+    """One rank of config 4's macro-mesh (level 3 here): per-tet residual norms of its own tets
+    (C oracle sweeps), aggregated by MacroMeshSmoother's SweepNorms (fixed-order local sum + one
+    allreduce per sweep) over gloo."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2210_15280_b200 import fitting, lattice, stencil
+    from paper_2210_15280_b200.partition import SweepNorms
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    level, sweeps = 3, 3
+    src = stencil.stencil_source(lattice.kuhn_tet((0, 1, 2)), level, stencil.CoefficientField.constant(1.0))
+    fit = fitting.fit_surrogate_ilu(src, level, (2, 2, 2), "v1")
+    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows)
+    mask = lattice.interior_mask(level)
+    agg = SweepNorms(sweeps, "cpu")
+    local = partition(384, world)[rank]
+    per_tet = np.zeros((sweeps, len(local)))
+    for i, t in enumerate(local):
+        u = np.zeros(lattice.grid_size(level))
+        u[mask] = np.random.default_rng(1000 + t).uniform(-1, 1, int(mask.sum()))
+        per_tet[:, i] = O.sweeps(sur, level, src.data, u, np.zeros_like(u), sweeps, return_norms=True)
+    for k in range(sweeps):
+        agg.add(k, torch.as_tensor(per_tet[k]))
+        agg.close_sweep(k)
+    q.put((rank, agg.result().tolist(), per_tet.sum(axis=1).tolist()))
+    dist.destroy_process_group()
+
+
+def test_macro_mesh_norm_aggregation_gloo_world2():
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sweepnorms_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g0, g1 = np.array(out[0][1]), np.array(out[1][1])
+    want = np.array(out[0][2]) + np.array(out[1][2])
+    assert np.array_equal(g0, g1)                     # every rank holds the same global norms
+    np.testing.assert_allclose(g0, want, rtol=1e-14)  # = sum over all 384 tets' norms
+    assert np.all(np.diff(g0) < 0)                     # the smoother decreases the residual

@@ -1,8 +1,9 @@
 """Time the single-tet sweep (plane kernels vs interleaved kernels) on one macro-tet.
 
-    LEVEL=9 Q=6 FAST=0 SWEEPS=10 python tools/plane_bench.py
+    LEVEL=9 Q=6 FAST=0 SWEEPS=10 COEF=sin python tools/plane_bench.py
 
-Unit tet, constant coefficient (config 3 geometry with k = 1), V1, u ~ U[-1, 1], f ~ N(0, 1).
+Unit tet, V1, u ~ U[-1, 1], f ~ N(0, 1); COEF=sin: config 3's k(x) with the rows evaluated on the
+fly (separable tables), COEF=one: constant coefficient.
 Prints ms/sweep and DoF-updates/s of tilu_sweep (pack + sweeps + unpack inside) and the per-kernel
 device times from the library's event profiler.
 """
@@ -24,7 +25,10 @@ sweeps = int(os.environ.get("SWEEPS", "10"))
 scheds = os.environ.get("SCHED", "plane").split(",")
 variant = os.environ.get("VARIANT", "v1")
 t0 = time.time()
-src = stencil.stencil_source(lattice.unit_tet(), level, stencil.CoefficientField.constant(1.0))
+coef = os.environ.get("COEF", "sin")
+src = stencil.stencil_source(lattice.unit_tet(), level,
+                             stencil.sin_kappa() if coef == "sin" else stencil.CoefficientField.constant(1.0))
+op = {"sepk": src.sepk} if src.sepk is not None else {"arow": src.data}
 fit = fitting.fit_surrogate_ilu(src, level, (q, q, q), variant)
 print(f"setup L{level}: {time.time() - t0:.1f}s eff {fit.degrees}", flush=True)
 N = lattice.interior_size(level)
@@ -35,8 +39,8 @@ u0[mask] = rng.uniform(-1, 1, int(mask.sum()))
 f0 = np.zeros_like(u0)
 f0[mask] = rng.normal(size=int(mask.sum()))
 for sched in scheds:
-    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, variant, fit.band_ranks, fit.store_rows, arow=src.data, fast=fast,
-                   schedule=sched)
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, variant, fit.band_ranks, fit.store_rows, fast=fast, schedule=sched,
+                   **op)
     u = torch.as_tensor(u0, device="cuda")
     f = torch.as_tensor(f0, device="cuda")
     p.sweep(u, f, 2)
