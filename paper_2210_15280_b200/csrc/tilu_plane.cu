@@ -436,18 +436,7 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                         mb_wait(&S.full[k][sl], (seq / NS) & 1);
                         PLN_ADD(2);
                     }
-                    // the group's helper values into registers at once (off the per-step chain), then
-                    // release the ring slot so the helpers refill it while the chain runs
                     const double *rg = &S.ring[k][sl][0][0][lane];
-                    double Lg[GS][7], rg_r[GS];
-#pragma unroll
-                    for (int j = 0; j < GS; ++j) {
-#pragma unroll
-                        for (int m = 0; m < 7; ++m) Lg[j][m] = rg[(j * 8 + m) * 32];
-                        rg_r[j] = rg[(j * 8 + 7) * 32];
-                    }
-                    __syncwarp();
-                    mb_arrive(&S.empty[k][sl]);
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         const int tau = tq + j;
@@ -483,7 +472,11 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                             lw2 = gl_on ? ga_prev : lw2;
                             lp1 = gl_on ? gb_cur : lp1;
                             lp2 = gl_on ? gb_prev : lp2;
-                            const double acc = fwd_chain<EXACT>(rg_r[j], Lg[j], w1, p1, p0, lw2, lw1, lp2, lp1);
+                            double L[7];
+#pragma unroll
+                            for (int m = 0; m < 7; ++m) L[m] = rg[(j * 8 + m) * 32];
+                            const double r = rg[(j * 8 + 7) * 32];
+                            const double acc = fwd_chain<EXACT>(r, L, w1, p1, p0, lw2, lw1, lp2, lp1);
                             const bool vpt = tau >= lo && tau <= hi;
                             const double wnew = vpt ? acc : 0.0;
                             if (p_on && k > 0) sts(hin + ((tau + 1) & (HR - 1)) * 32, sentv());
@@ -499,6 +492,7 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                             prefetch();
                         }
                     }
+                    mb_arrive(&S.empty[k][sl]);
                     ++seq;
                 };
                 for (int q = 0; q < ngroups; ++q) grp(q);
@@ -753,21 +747,8 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                     if (hout) wait_armed(hout, tq, -1, T0 - 1, T1 - 1);
                     mb_wait(&S.tfull[k][tsl], (tseq / NT) & 1);
                     mb_wait(&S.full[k][sl], (seq / NS) & 1);
-                    // the group's helper values and staged w_f / u into registers at once (off the chain);
-                    // release the helper ring slot right away
                     const double *rg = &S.ring[k][sl][0][0][lane];
                     const double *tb = reinterpret_cast<const double *>(S.tbuf[k][tsl]) + lane + 1;
-                    double Lg[GS][7], rg_d[GS], wfg[GS], ug[GS];
-#pragma unroll
-                    for (int j = 0; j < GS; ++j) {
-#pragma unroll
-                        for (int m = 0; m < 7; ++m) Lg[j][m] = rg[(j * 8 + m) * 32];
-                        rg_d[j] = rg[(j * 8 + 7) * 32];
-                        wfg[j] = tb[(GS - 1 - j) * WIN];          // line of tau = tq - j in the boxes
-                        ug[j] = tb[UOFF + (GS - 1 - j) * WIN];
-                    }
-                    __syncwarp();
-                    mb_arrive(&S.empty[k][sl]);
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         const int tau = tq - j;
@@ -803,8 +784,13 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                             lw2 = gl_on ? ga_prev : lw2;
                             lq1 = gl_on ? gb_cur : lq1;
                             lq2 = gl_on ? gb_prev : lq2;
-                            const double uv = ug[j];
-                            const double acc = bwd_chain<EXACT>(rg_d[j], wfg[j], Lg[j], wb1, q1, q0, lw2, lw1, lq2, lq1);
+                            const double wfv = tb[(GS - 1 - j) * WIN];          // line of tau in the boxes
+                            const double uv = tb[UOFF + (GS - 1 - j) * WIN];
+                            double Lq[7];
+#pragma unroll
+                            for (int m = 0; m < 7; ++m) Lq[m] = rg[(j * 8 + m) * 32];
+                            const double inv_d = rg[(j * 8 + 7) * 32];
+                            const double acc = bwd_chain<EXACT>(inv_d, wfv, Lq, wb1, q1, q0, lw2, lw1, lq2, lq1);
                             const bool vpt = tau >= lo && tau <= hi;
                             const double wnew = vpt ? acc : 0.0;
                             if (q_on && k > 0) sts(hin + ((tau - 1) & (HR - 1)) * 32, sentv());
@@ -823,6 +809,7 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                     }
                     __syncwarp();
                     if (lane == 0 && q + NT < ngroups) issue(q + NT);
+                    mb_arrive(&S.empty[k][sl]);
                     ++seq;
                     ++tseq;
                 };

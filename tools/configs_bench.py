@@ -20,6 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
+import bench  # noqa: E402  (roofline model: SURVEY 8(d) fixed bytes / ops per DoF, measured peaks)
 from oracle import oracle as O  # noqa: E402
 from paper_2210_15280_b200 import CellILU, DevicePlan, _lib, fitting, lattice, stencil  # noqa: E402
 
@@ -81,6 +82,13 @@ def one(cfg, level, q, verts, coeff, sweeps, src=None, stored=False):
            "max_rel_err_vs_oracle": float(np.abs(ug - uo).max() / np.abs(uo).max()),
            "bitwise_vs_oracle": bool(np.array_equal(ug, uo)),
            "stencil": "constant row" if src.constant else "per-point rows"}
+    bpd = bench.algo_bytes(level, "v1")["sweep"]
+    opd = bench.algo_ops(level, fit.degrees)
+    rt = bench.roofline_time(N, bpd, opd)
+    t_roof = max(rt["t_hbm_s"], rt["t_fp64_s"])
+    rec["roofline"] = {"bound": rt["bound"], "algorithmic_bytes_per_dof": bpd, "algorithmic_fp64_ops_per_dof": opd,
+                       "t_roofline_ms": t_roof * 1e3, "frac": t_roof / (ms / 1e3), "hbm_gbs": rt["hbm_gbs"],
+                       "fp64_tflops": rt["fp64_tflops"]}
     if stored:
         fr = fitting.factorize_tet(src, level, full_store=True)
         cplan = CellILU(fr).plan(**op)
@@ -96,6 +104,11 @@ def one(cfg, level, q, verts, coeff, sweeps, src=None, stored=False):
         sms = e0.elapsed_time(e1) / 5
         rec["stored_ilu_ms_per_sweep"] = sms
         rec["stored_ilu_dof_updates_per_s"] = N / (sms / 1e3)
+        # K4: 48 B vectors + 7 L (fwd) + 7 transposed L and 1/D (bwd) = 168 B/DoF, 60 ops
+        rk = bench.roofline_time(N, 168.0, 60.0)
+        tk = max(rk["t_hbm_s"], rk["t_fp64_s"])
+        rec["stored_ilu_roofline"] = {"bound": rk["bound"], "algorithmic_bytes_per_dof": 168.0,
+                                      "t_roofline_ms": tk * 1e3, "frac": tk / (sms / 1e3)}
     return rec, src
 
 
