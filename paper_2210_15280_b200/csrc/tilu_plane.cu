@@ -79,6 +79,7 @@ constexpr int HR = TILU_PLANE_HR;  // solver -> solver handoff ring depth (steps
 #endif
 constexpr int PD = TILU_PLANE_PD;  // global handoff prefetch distance (steps), power of two
 constexpr int WIN = 34;  // doubles per staged line: z0-1 .. z0+32
+constexpr int RS = 10;   // doubles per lane and step in the helper -> solver ring (8 used; 80-byte stride)
 // one staged group: forward u box [3 planes s-1..s+1][GS+4 lines][WIN] + f box [GS][WIN];
 // backward w_f box [GS][WIN] + u box [GS][WIN]  (tensor copies need 128-byte aligned destinations)
 constexpr int FOFF = (3 * (GS + 4) * WIN * 8 + 127) / 128 * 128 / 8;  // doubles: f box offset in a slot
@@ -118,6 +119,7 @@ struct Args {
     double *part;          // [ntasks][PW * 32] residual partial sums (forward) or nullptr
     long long *steplog;    // TILU_PLANE_STEPLOG: [PW][2048] clock64 at every step of task 0 (or nullptr)
     long long *trace;      // TILU_PLANE_TRACE: [ntasks][4] = start ns, end ns, sm id, CTA (or nullptr)
+    int prof_task;         // TILU_PLANE_PROF builds: ticket whose warps the steplog measures (TILU_PLANE_PROF_TASK)
     Geo g;
     int stored;            // 1: L / 1/D from the stored ILU(0) factors (CellILU, ilu.py:210-227) instead of NDDF
     double arow[15];       // constant stencil (kernel-parameter bank)
@@ -202,8 +204,9 @@ __device__ __forceinline__ int band_off(int x, int y, int z) { return (z == 1 ||
 // Shared memory of one CTA.
 struct Smem {
     alignas(128) unsigned char tbuf[PW][NT][TSLOT];  // TMA ring (groups of GS steps)
-    double ring[PW][NS][GS][8][32];                 // helpers -> solver: per step 7 L values + residual (fwd)
-                                                    // or 7 source-point L values + 1/D (bwd)
+    double ring[PW][NS][GS][32][RS];                // helpers -> solver: per step and lane 7 L values + residual
+                                                    // (fwd) or 7 source-point L values + 1/D (bwd); RS = 10
+                                                    // keeps the solver's four 16-byte loads conflict-free
     double hring[PW][HR][32];                       // solver k-1 -> solver k handoff ring
     double pre[PW][PD][3][32];                      // prefetched global handoff values (cp.async)
     uint64_t tfull[PW][NT];                         // TMA group landed
@@ -377,8 +380,8 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
         const int ngroups = (T1 - T0) / GS + 1;
         double r2 = 0.0;
 #ifdef TILU_PLANE_PROF
-        const bool prof = A.steplog && t == 0;
-        long long pc[6] = {0, 0, 0, 0, 0, 0};
+        const bool prof = A.steplog && t == A.prof_task;
+        long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         const long long pstart = prof ? clock64() : 0;
 #endif
         if (role == 0) {
@@ -392,35 +395,41 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                     if (hout && tau >= T0 + 1) put_s(hout + (tau & (HR - 1)) * 32, 0.0);
                 }
             } else {
-                // warp 0: P(tau+1) = w_f(s-1, tau+1, z); lane 0: ga = w_f(s, tau-1, z0-1), gb = w_f(s-1, tau, z0-1)
-                const double *pw0 = A.W + pidx(g, s - 1, 1, z);
-                const double *pga = A.W + pidx(g, s, -1, z0 - 1);
-                const double *pgb = A.W + pidx(g, s - 1, 0, z0 - 1);
-                double *pwo = A.W + pidx(g, s, 0, z);
-                double *pbo = A.B + pidx(g, s, 0, z);
-                const bool gp_on = (k == 0), gl_on = (lane == 0);
+                // Lean step: every solver reads its predecessor value p0 = (s-1, tau+1, z) from its input
+                // ring hring[k] -- for k > 0 written by solver k-1, for k == 0 (no predecessor in the band)
+                // filled by cp.async from the band below's w_f plane PD steps ahead (zeros for band 0) --
+                // so the fast path is one shared-memory load and one vote for every warp; lane 0 also
+                // takes ga = w_f(s, tau-1, z0-1), gb = w_f(s-1, tau, z0-1) of the chunk below (prefetched
+                // into pre[k]).  No branches on the fast path; sentinels (producer not there yet) go to
+                // the re-poll loop.
+                const bool gl_on = (lane == 0);
                 // the global inputs can only be nonzero when the band below (b > 0) / the chunk below (c > 0)
                 // exists: otherwise they are boundary zeros and are neither fetched nor polled
-                const bool gp_ld = gp_on && b > 0, gl_ld = gl_on && z0 > 1;
-                // global handoff inputs of step tau, prefetched PD steps ahead into pre[k][tau & (PD-1)]
-                // (addresses of out-of-range steps stay inside the allocation and read boundary zeros)
-                double *pre = &S.pre[k][0][0][lane];
-                const uint32_t pre_s = su32(pre);
-                // running source pointers of the prefetch stream (step tn = next step to prefetch)
-                const double *nw0 = pw0 + T0 * ZP, *nga = pga + T0 * ZP, *ngb = pgb + T0 * ZP;
-                int tn = T0;
-                auto prefetch = [&]() {
-                    const uint32_t d = pre_s + (uint32_t)((tn & (PD - 1)) * 96 * 8);
-                    if (gp_ld) cpa8(d, nw0);
+                const bool gp_ld = (k == 0) && b > 0, gl_ld = gl_on && z0 > 1;
+                const double *pw0 = A.W + pidx(g, s - 1, 1, z);        // P(tau+1) = pw0[tau * ZP]
+                const double *pga = A.W + pidx(g, s, -1, z0 - 1);      // ga(tau) = pga[tau * ZP]
+                const double *pgb = A.W + pidx(g, s - 1, 0, z0 - 1);   // gb(tau) = pgb[tau * ZP]
+                double *pwo = A.W + pidx(g, s, 0, z);
+                double *pbo = A.B + pidx(g, s, 0, z);
+                if (k == 0) {  // band input ring: boundary zeros (band 0), else overwritten by the prefetch
+#pragma unroll
+                    for (int e = 0; e < HR; ++e) hin[e * 32] = 0.0;
+                    __syncwarp();
+                }
+                const uint32_t hin_s = su32(hin), pre_s = su32(&S.pre[k][0][0][lane]);
+                // global inputs of step tn, PD steps ahead (addresses of out-of-range steps stay inside the
+                // allocation and read boundary zeros)
+                auto prefetch = [&](const int tn) {
+                    if (gp_ld) cpa8(hin_s + (uint32_t)(((tn + 1) & (HR - 1)) * 32 * 8), pw0 + (int64_t)tn * ZP);
                     if (gl_ld) {
-                        cpa8(d + 32 * 8, nga);
-                        cpa8(d + 64 * 8, ngb);
+                        const uint32_t d = pre_s + (uint32_t)((tn & (PD - 1)) * 96 * 8);
+                        cpa8(d + 32 * 8, pga + (int64_t)tn * ZP);
+                        cpa8(d + 64 * 8, pgb + (int64_t)tn * ZP);
                     }
                     cpa_commit();
-                    nw0 += ZP; nga += ZP; ngb += ZP; ++tn;
                 };
-                for (int i = 0; i < PD; ++i) prefetch();
-                double *wo = pwo + T0 * ZP, *bo = pbo + T0 * ZP;  // own w_f / w_b handoff position at tau
+#pragma unroll
+                for (int i = 0; i < PD; ++i) prefetch(T0 + i);
                 double w1 = 0, w2 = 0, p1 = 0, p2 = 0, ga_prev = 0, gb_prev = 0;
                 const bool rearm_b = live && (k == 0 || (lane == 0 && z0 > 32));
                 auto grp = [&](const int q) {
@@ -436,34 +445,39 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                         mb_wait(&S.full[k][sl], (seq / NS) & 1);
                         PLN_ADD(2);
                     }
-                    const double *rg = &S.ring[k][sl][0][0][lane];
+                    const double *rg = &S.ring[k][sl][0][lane][0];
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         const int tau = tq + j;
                         if (tau <= T1) {
+#ifdef TILU_PLANE_PROF
+                            const long long _s0 = prof ? clock64() : 0;
+#endif
                             const bool p_on = tau <= T1 - 1;
-                            double p0 = 0.0;
                             cpa_wait_pd();
-                            const double *pv = pre + (tau & (PD - 1)) * 96;
-                            if (p_on) p0 = gp_on ? (gp_ld ? pv[0] : 0.0) : lds_vol(hin + ((tau + 1) & (HR - 1)) * 32);
+                            double *hs = hin + ((tau + 1) & (HR - 1)) * 32;
+                            const double *pv = &S.pre[k][tau & (PD - 1)][0][lane];
+                            double p0 = p_on ? lds_vol(hs) : 0.0;
                             double ga_cur = gl_ld ? pv[32] : 0.0, gb_cur = gl_ld ? pv[64] : 0.0;
-                            // acquire: inputs produced by other warps must be final before the chain runs
-                            if (__any_sync(0xffffffffu,
-                                           p_on && (is_sent(p0) || (gl_ld && (is_sent(ga_cur) || is_sent(gb_cur)))))) {
+                            // acquire: inputs produced by other warps / CTAs must be final before the chain
+                            bool wt = p_on && (is_sent(p0) || is_sent(ga_cur) || is_sent(gb_cur));
+                            if (__builtin_expect(__any_sync(0xffffffffu, wt), 0)) {
                                 long long spins = 0;
-                                for (;;) {
-                                    if (p_on && is_sent(p0)) p0 = gp_on ? ldg_cg(pw0 + tau * ZP)
-                                                                        : lds_vol(hin + ((tau + 1) & (HR - 1)) * 32);
-                                    if (gl_ld && p_on) {
-                                        if (is_sent(ga_cur)) ga_cur = ldg_cg(pga + tau * ZP);
-                                        if (is_sent(gb_cur)) gb_cur = ldg_cg(pgb + tau * ZP);
-                                    }
-                                    const bool still =
-                                        p_on && (is_sent(p0) || (gl_ld && (is_sent(ga_cur) || is_sent(gb_cur))));
-                                    if (!__any_sync(0xffffffffu, still)) break;
+                                do {
+                                    if (is_sent(p0)) p0 = (k == 0) ? ldg_cg(pw0 + (int64_t)tau * ZP) : lds_vol(hs);
+                                    if (is_sent(ga_cur)) ga_cur = ldg_cg(pga + (int64_t)tau * ZP);
+                                    if (is_sent(gb_cur)) gb_cur = ldg_cg(pgb + (int64_t)tau * ZP);
+                                    wt = is_sent(p0) || is_sent(ga_cur) || is_sent(gb_cur);
                                     if (++spins > (1ll << 26)) __trap();
-                                }
+                                } while (__any_sync(0xffffffffu, wt));
                             }
+#ifdef TILU_PLANE_PROF
+                            long long _s1 = 0;
+                            if (prof) {
+                                asm volatile("mov.u64 %0, %%clock64;" : "=l"(_s1) : "d"(p0), "d"(ga_cur), "d"(gb_cur));
+                                pc[4] += _s1 - _s0;
+                            }
+#endif
                             double lw1 = __shfl_up_sync(0xffffffffu, w1, 1);
                             double lw2 = __shfl_up_sync(0xffffffffu, w2, 1);
                             double lp1 = __shfl_up_sync(0xffffffffu, p1, 1);
@@ -472,24 +486,33 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                             lw2 = gl_on ? ga_prev : lw2;
                             lp1 = gl_on ? gb_cur : lp1;
                             lp2 = gl_on ? gb_prev : lp2;
-                            double L[7];
-#pragma unroll
-                            for (int m = 0; m < 7; ++m) L[m] = rg[(j * 8 + m) * 32];
-                            const double r = rg[(j * 8 + 7) * 32];
-                            const double acc = fwd_chain<EXACT>(r, L, w1, p1, p0, lw2, lw1, lp2, lp1);
+                            // the step's seven L values and residual: four 16-byte loads
+                            const double2 *r2 = reinterpret_cast<const double2 *>(rg + j * (32 * RS));
+                            const double2 a0 = r2[0], a1 = r2[1], a2 = r2[2], a3 = r2[3];
+                            const double L[7] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x};
+                            const double acc = fwd_chain<EXACT>(a3.y, L, w1, p1, p0, lw2, lw1, lp2, lp1);
                             const bool vpt = tau >= lo && tau <= hi;
                             const double wnew = vpt ? acc : 0.0;
-                            if (p_on && k > 0) sts(hin + ((tau + 1) & (HR - 1)) * 32, sentv());
+#ifdef TILU_PLANE_PROF
+                            long long _s2 = 0;
+                            if (prof) {
+                                asm volatile("mov.u64 %0, %%clock64;" : "=l"(_s2) : "d"(wnew));
+                                pc[5] += _s2 - _s1;
+                            }
+#endif
+                            if (p_on && k > 0) sts(hs, sentv());                    // re-arm the input slot
                             if (hout && tau >= T0 + 1) sts(hout + (tau & (HR - 1)) * 32, wnew);
                             if (vpt) {
-                                st_rlx(wo, wnew);                 // polled by the next band / chunk
-                                if (rearm_b) st_rlx(bo, sentv());
+                                st_rlx(pwo + (int64_t)tau * ZP, wnew);             // polled by the next band / chunk
+                                if (rearm_b) st_rlx(pbo + (int64_t)tau * ZP, sentv());
                             }
-                            wo += ZP; bo += ZP;
                             ga_prev = ga_cur; gb_prev = gb_cur;
                             w2 = w1; w1 = wnew;
                             p2 = p1; p1 = p0;
-                            prefetch();
+                            prefetch(tau + PD);
+#ifdef TILU_PLANE_PROF
+                            if (prof) pc[6] += clock64() - _s2;
+#endif
                         }
                     }
                     mb_arrive(&S.empty[k][sl]);
@@ -544,14 +567,14 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                     mb_wait(&S.empty[k][sl], ((seq / NS) & 1) ^ 1);
                     PLN_ADD(2);
                 }
-                double *rg = &S.ring[k][sl][0][0][lane];
+                double *rg = &S.ring[k][sl][0][lane][0];
 #pragma unroll
                 for (int j = 0; j < GS; ++j) {
                     const int tau = tq + j;
                     const bool vpt = tau >= lo && tau <= hi;
                     const bool isb = stored || (v1 && vpt && (rowband || tau == lo || tau == hi));
 #pragma unroll
-                    for (int m = 0; m < 7; ++m) rg[(j * 8 + m) * 32] = isb ? bl[j][m] : d[m][0];
+                    for (int m = 0; m < 7; ++m) rg[j * (32 * RS) + m] = isb ? bl[j][m] : d[m][0];
                     if (vpt && !stored) {
 #pragma unroll
                         for (int m = 0; m < 7; ++m) march<K>(d[m]);
@@ -595,7 +618,7 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                     mb_wait(&S.empty[k][sl], ((seq / NS) & 1) ^ 1);
                     PLN_ADD(2);
                 }
-                double *rg = &S.ring[k][sl][0][0][lane];
+                double *rg = &S.ring[k][sl][0][lane][0];
 #pragma unroll
                 for (int j = 0; j < GS; ++j) {
                     const int sg = tq + j;
@@ -638,7 +661,7 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                         res = dsub(tb[FOFF], out);
                         r2 = fma(res, res, r2);
                     }
-                    rg[(j * 8 + 7) * 32] = res;
+                    rg[j * (32 * RS) + 7] = res;
                 }
                 __syncwarp();
                 if (lane == 0 && q + NT < ngroups) issue(q + NT);
@@ -652,6 +675,8 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
             sl[0] += clock64() - pstart;
             for (int i = 1; i < 5; ++i) sl[i] += pc[i];
             sl[5] += ngroups;
+            sl[6] += pc[5];
+            sl[7] += pc[6];
         }
 #endif
         __syncthreads();
@@ -747,7 +772,7 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                     if (hout) wait_armed(hout, tq, -1, T0 - 1, T1 - 1);
                     mb_wait(&S.tfull[k][tsl], (tseq / NT) & 1);
                     mb_wait(&S.full[k][sl], (seq / NS) & 1);
-                    const double *rg = &S.ring[k][sl][0][0][lane];
+                    const double *rg = &S.ring[k][sl][0][lane][0];
                     const double *tb = reinterpret_cast<const double *>(S.tbuf[k][tsl]) + lane + 1;
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
@@ -788,8 +813,8 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                             const double uv = tb[UOFF + (GS - 1 - j) * WIN];
                             double Lq[7];
 #pragma unroll
-                            for (int m = 0; m < 7; ++m) Lq[m] = rg[(j * 8 + m) * 32];
-                            const double inv_d = rg[(j * 8 + 7) * 32];
+                            for (int m = 0; m < 7; ++m) Lq[m] = rg[j * (32 * RS) + m];
+                            const double inv_d = rg[j * (32 * RS) + 7];
                             const double acc = bwd_chain<EXACT>(inv_d, wfv, Lq, wb1, q1, q0, lw2, lw1, lq2, lq1);
                             const bool vpt = tau >= lo && tau <= hi;
                             const double wnew = vpt ? acc : 0.0;
@@ -910,15 +935,15 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                 const int sl = seq % NS;
                 const int tq = T1 - GS * q;
                 mb_wait(&S.empty[k][sl], ((seq / NS) & 1) ^ 1);
-                double *rg = &S.ring[k][sl][0][0][lane];
+                double *rg = &S.ring[k][sl][0][lane][0];
 #pragma unroll
                 for (int j = 0; j < GS; ++j) {
                     const int tau = tq - j;
                     const unsigned im = bim[j], bm = bbm[j];
 #pragma unroll
                     for (int m = 0; m < 7; ++m)
-                        rg[(j * 8 + m) * 32] = ((im >> m) & 1u) ? (((bm >> m) & 1u) ? bl[j][m] : d[m][0]) : 0.0;
-                    rg[(j * 8 + 7) * 32] = ((bm >> 7) & 1u) ? bl[j][7] : d[7][0];
+                        rg[j * (32 * RS) + m] = ((im >> m) & 1u) ? (((bm >> m) & 1u) ? bl[j][m] : d[m][0]) : 0.0;
+                    rg[j * (32 * RS) + 7] = ((bm >> 7) & 1u) ? bl[j][7] : d[7][0];
                     if (tau >= lo && tau <= hi && !stored) {
 #pragma unroll
                         for (int m = 0; m < 8; ++m) march<K>(d[m]);
@@ -1257,6 +1282,10 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
         A.part = rnorm2 ? w->part : nullptr;
         A.trace = w->trace;
         A.steplog = w->steplog;
+        {
+            static const char *pt = std::getenv("TILU_PLANE_PROF_TASK");
+            A.prof_task = pt ? std::atoi(pt) : 0;
+        }
         prof_begin(s);
         bool ok = launch_pass(P, A, w->maps, w->ctas, exact, true, s);
         prof_end("plane_fwd", s);
@@ -1285,10 +1314,10 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
         std::vector<long long> h(3 * PW * 8);
         cudaMemcpy(h.data(), w->steplog, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
         if (FILE *fp = std::fopen(steplog_path, "w")) {
-            std::fprintf(fp, "warp total armed ringwait tmawait slowpath groups\n");
+            std::fprintf(fp, "warp total armed ringwait tmawait acquire groups chain tail\n");
             for (int wv = 0; wv < 3 * PW; ++wv) {
                 std::fprintf(fp, "%d", wv);
-                for (int i = 0; i < 6; ++i) std::fprintf(fp, " %lld", h[wv * 8 + i]);
+                for (int i = 0; i < 8; ++i) std::fprintf(fp, " %lld", h[wv * 8 + i]);
                 std::fprintf(fp, "\n");
             }
             std::fclose(fp);
