@@ -225,19 +225,7 @@ __device__ __forceinline__ void ready(Vt<T> &v, const double *p)
 __device__ __forceinline__ bool in_band_b(int x, int y, int z, int xe) { return z == 1 || y == 1 || x == 1 || x == xe; }
 
 
-// Debug build (-DTILU_DEBUG_BOUNDS): every packed / table access is range-checked.
-#ifdef TILU_DEBUG_BOUNDS
-#define TILU_CHECK(cond, what, a, b)                                                                  \
-    do {                                                                                              \
-        if (!(cond)) {                                                                                \
-            printf("tilu bounds: %s (%lld, %lld) block %d thread %d\n", what, (long long)(a), (long long)(b), \
-                   blockIdx.x, threadIdx.x);                                                          \
-            __trap();                                                                                 \
-        }                                                                                             \
-    } while (0)
-#else
-#define TILU_CHECK(cond, what, a, b) ((void)0)
-#endif
+// TILU_CHECK (tilu_common.cuh): packed / table accesses are range-checked in -DTILU_DEBUG_BOUNDS builds.
 
 // 8 coefficients of one point (uniform address across the warp: one broadcast transaction each).
 __device__ __forceinline__ void ld_coef(double (&c)[8], const double *p)
@@ -1005,6 +993,7 @@ void launch_arm(const PlanDev &P, double *wa, const unsigned long long *hdr, uns
 }
 
 // Persistent grid: as many CTAs as fit on the device at once (queried once per kernel).
+constexpr int kMaxDevices = 64;
 template <class Kern>
 static unsigned persistent_grid(Kern k, size_t smem)
 {
@@ -1021,7 +1010,13 @@ static void launch_fwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_
 {
     constexpr size_t sm = ring_smem<kFwdNS, T, kStages<T>>();
     auto run = [&](auto kern) {
-        static const unsigned grid = persistent_grid(kern, sm);
+        // the smem attribute and the resident grid are per device: cached per device ordinal
+        static unsigned grids[kMaxDevices] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= kMaxDevices) dev = 0;
+        if (!grids[dev]) grids[dev] = persistent_grid(kern, sm);
+        const unsigned grid = grids[dev];
         A.nwarps = (int)grid * kWarps;
         kern<<<grid, kWarps * 32, sm, s>>>(P, A);
     };
@@ -1040,7 +1035,13 @@ static void launch_bwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_
 {
     constexpr size_t sm = ring_smem<kBwdNS, T, kStages<T>>();
     auto run = [&](auto kern) {
-        static const unsigned grid = persistent_grid(kern, sm);
+        // the smem attribute and the resident grid are per device: cached per device ordinal
+        static unsigned grids[kMaxDevices] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= kMaxDevices) dev = 0;
+        if (!grids[dev]) grids[dev] = persistent_grid(kern, sm);
+        const unsigned grid = grids[dev];
         A.nwarps = (int)grid * kWarps;
         kern<<<grid, kWarps * 32, sm, s>>>(P, A);
     };

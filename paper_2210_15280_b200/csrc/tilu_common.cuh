@@ -3,6 +3,23 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Debug build (-DTILU_DEBUG_BOUNDS, tools/build_variant.py bounds -DTILU_DEBUG_BOUNDS): global-memory
+// indices of every kernel family are range-checked; a violation prints and traps.  Off (no code) in
+// the product build.
+#ifdef TILU_DEBUG_BOUNDS
+#include <cstdio>
+#define TILU_CHECK(cond, what, a, b)                                                                  \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("tilu bounds: %s (%lld, %lld) block %d thread %d\n", what, (long long)(a), (long long)(b), \
+                   blockIdx.x, threadIdx.x);                                                          \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define TILU_CHECK(cond, what, a, b) ((void)0)
+#endif
+
 namespace tilu {
 
 // Unfused IEEE fp64 ops.  The reference Numba kernels contract nothing; the

@@ -120,6 +120,7 @@ struct Args {
     long long *steplog;    // TILU_PLANE_STEPLOG: [PW][2048] clock64 at every step of task 0 (or nullptr)
     long long *trace;      // TILU_PLANE_TRACE: [ntasks][4] = start ns, end ns, sm id, CTA (or nullptr)
     int prof_task;         // TILU_PLANE_PROF builds: ticket whose warps the steplog measures (TILU_PLANE_PROF_TASK)
+    int64_t pe;            // doubles per plane vector (bounds checks of -DTILU_DEBUG_BOUNDS builds)
     Geo g;
     int stored;            // 1: L / 1/D from the stored ILU(0) factors (CellILU, ilu.py:210-227) instead of NDDF
     double arow[15];       // constant stencil (kernel-parameter bank)
@@ -420,6 +421,10 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                 // global inputs of step tn, PD steps ahead (addresses of out-of-range steps stay inside the
                 // allocation and read boundary zeros)
                 auto prefetch = [&](const int tn) {
+                    TILU_CHECK(!gp_ld || (pw0 + (int64_t)tn * ZP - A.W >= 0 && pw0 + (int64_t)tn * ZP - A.W < A.pe),
+                               "plane fwd band input", tn, s);
+                    TILU_CHECK(!gl_ld || (pga + (int64_t)tn * ZP - A.W >= 0 && pgb + (int64_t)tn * ZP - A.W < A.pe),
+                               "plane fwd chunk input", tn, s);
                     if (gp_ld) cpa8(hin_s + (uint32_t)(((tn + 1) & (HR - 1)) * 32 * 8), pw0 + (int64_t)tn * ZP);
                     if (gl_ld) {
                         const uint32_t d = pre_s + (uint32_t)((tn & (PD - 1)) * 96 * 8);
@@ -503,6 +508,8 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                             if (p_on && k > 0) sts(hs, sentv());                    // re-arm the input slot
                             if (hout && tau >= T0 + 1) sts(hout + (tau & (HR - 1)) * 32, wnew);
                             if (vpt) {
+                                TILU_CHECK(pwo + (int64_t)tau * ZP - A.W >= 0 && pwo + (int64_t)tau * ZP - A.W < A.pe,
+                                           "plane fwd w_f store", tau, s);
                                 st_rlx(pwo + (int64_t)tau * ZP, wnew);             // polled by the next band / chunk
                                 if (rearm_b) st_rlx(pbo + (int64_t)tau * ZP, sentv());
                             }
@@ -551,6 +558,9 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                 const bool isb = stored ? vp : (v1 && vp && (rowband || tau == lo || tau == hi));
                 const double *st = stored ? P.factors + 9 * (rbase + x)
                                           : P.store + 9 * (int64_t)(boff + (rowband ? x - 1 : (tau == lo ? 0 : 1)));
+                TILU_CHECK(!isb || (stored ? (rbase + x >= 0 && rbase + x < P.grid)
+                                           : (boff + (rowband ? x - 1 : (tau == lo ? 0 : 1)) < P.nband_dbg)),
+                           "plane fwd band / factor row", tau, z);
                 if (__any_sync(0xffffffffu, isb)) {
 #pragma unroll
                     for (int m = 0; m < 7; ++m) v[m] = ld_if(isb, st + m, 0.0);
@@ -638,6 +648,7 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
 #pragma unroll
                             for (int qq = 0; qq < 15; ++qq) a[qq] = A.arow[qq];
                         } else {
+                            TILU_CHECK(rbase + (sg - z) >= 0 && rbase + (sg - z) < P.grid, "plane residual row", sg, z);
                             const double *ar = P.arows + 15 * (rbase + (sg - z));
 #pragma unroll
                             for (int qq = 0; qq < 15; ++qq) a[qq] = ar[qq];
@@ -821,6 +832,7 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                             if (q_on && k > 0) sts(hin + ((tau - 1) & (HR - 1)) * 32, sentv());
                             if (hout && tau <= T1 - 1) sts(hout + (tau & (HR - 1)) * 32, wnew);
                             if (vpt) {
+                                TILU_CHECK(uo - A.u >= 0 && uo - A.u < A.pe, "plane bwd u store", tau, s);
                                 *uo = dadd(uv, acc);
                                 if (b_out) st_rlx(bo, acc);       // polled by the band / chunk below
                                 if (rearm_w) st_rlx(wo, sentv());
@@ -1108,8 +1120,13 @@ static cudaError_t set_attrs()
 template <int K, bool EXACT, int AMODE>
 static bool launch_k(const PlanDev &P, const Args &A, const Maps &M, int ctas, bool fwd, cudaStream_t s)
 {
-    static bool attrs = (set_attrs<K, EXACT, AMODE>() == cudaSuccess);
-    if (!attrs) return false;
+    // the dynamic shared-memory attribute belongs to a device context: set once per device ordinal
+    static signed char attrs[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!attrs[dev]) attrs[dev] = (set_attrs<K, EXACT, AMODE>() == cudaSuccess) ? 1 : -1;
+    if (attrs[dev] < 0) return false;
     if (fwd) k_plane_fwd<K, EXACT, AMODE><<<ctas, 3 * PW * 32, sizeof(Smem), s>>>(P, A, M);
     else k_plane_bwd<K, EXACT><<<ctas, 2 * PW * 32, sizeof(Smem), s>>>(P, A, M);
     return true;
@@ -1255,6 +1272,7 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
     A.tasks = w->tasks;
     A.ntasks = w->ntasks;
     A.g = w->g;
+    A.pe = plane_elems(w->g);
     std::memcpy(A.arow, p->harow, sizeof(A.arow));
     A.stored = stored ? 1 : 0;
     if (stored && !p->dev.factors) return TILU_EINVAL;

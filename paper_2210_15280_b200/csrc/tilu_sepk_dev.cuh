@@ -13,6 +13,7 @@ namespace tilu {
 // v[i] = tab[c + i - 3], i = 0..6 (tables hold 4n + 1 abscissae; c = 4 * coordinate, 1 <= coordinate <= n - 3)
 __device__ __forceinline__ void sepk_window(const double *__restrict__ tab, int c, double (&v)[7])
 {
+    TILU_CHECK(c >= 4, "sepk window", c, 0);
 #pragma unroll
     for (int i = 0; i < 7; ++i) v[i] = __ldg(tab + c + i - 3);
 }

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(128) k_residual(PlanDev P, const double *__res
     double ss = 0.0;
     for (int x = 1 + threadIdx.x; x <= ri.xe; x += blockDim.x) {
         const int64_t p = base + x;
+        TILU_CHECK(p >= 0 && p < P.grid && rs + x + 1 < P.grid && rtc + x < P.grid, "residual point", p, P.grid);
         double sa[15];
         if (AMODE == 2) sepk_point(P, x, y, z, sa);
         const double *a = AMODE == 2 ? sa : AMODE == 1 ? P.arow : P.arows + 15 * p;

@@ -1,8 +1,10 @@
-"""Small invocations of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck):
-    compute-sanitizer --tool memcheck python tools/sanitize_cases.py
+"""Small invocations of every kernel family, for the bounds-checked build (compute-sanitizer is not
+available on the GPU pool):
+    python tools/build_variant.py bounds -DTILU_DEBUG_BOUNDS
+    TILU_LIB=paper_2210_15280_b200/lib/variants/libtilu_bounds.so python tools/small_cases.py
 reference-layout (simple) kernels, plane-layout band kernels (const row, per-point rows, on-the-fly
 separable rows, stored factors), batched dataflow kernels (1 and 2 tets per lane), residual /
-stencil apply / operator surrogate.  Levels 3-5 keep the sanitizer runs to minutes."""
+stencil apply / operator surrogate, levels 3-5."""
 import os
 import sys
 
