@@ -238,56 +238,40 @@ __device__ __forceinline__ double ld_if(bool p, const double *ptr, double other)
     return v;
 }
 
-// Forward substitution of one point: reference order w s se bnw bn bc be (_kernels.py:350-364), or
-// (fast) FMA with the newest operands (own row, same-diagonal lane) last.
+// The substitution split around the acquire of the step's handoff inputs (forward: p0 = (s-1, tau+1, z)
+// and lane z-1's lw1, lp1, which lane 0 takes from the chunk below; backward, mirrored: q0 from diagonal
+// s+1 and lane z+1's values): the terms of values already in registers are evaluated first.  Both
+// passes have the same shape.  Exact mode keeps the reference order -- forward r - L_w w1 - L_s p1 - L_se p0
+// - L_bnw lw2 - L_bn lw1 - L_bc lp2 - L_be lp1 (_kernels.py:350-364), backward r = inv_d w_f then the
+// seven source points in the same slots (_kernels.py:416-428) -- the products are computed early but
+// every subtraction happens in the same order, so the result is bitwise the reference's; fast mode
+// subtracts the earlier inputs first and the step's inputs last with FMA.
 template <bool EXACT>
-__device__ __forceinline__ double fwd_chain(double r, const double (&L)[7], double w1, double p1, double p0, double lw2,
-                                            double lw1, double lp2, double lp1)
-{
-    double acc = r;
-    if (EXACT) {
-        acc = msub<true>(acc, L[0], w1);
-        acc = msub<true>(acc, L[1], p1);
-        acc = msub<true>(acc, L[2], p0);
-        acc = msub<true>(acc, L[3], lw2);
-        acc = msub<true>(acc, L[4], lw1);
-        acc = msub<true>(acc, L[5], lp2);
-        acc = msub<true>(acc, L[6], lp1);
-    } else {
-        acc = msub<false>(acc, L[1], p1);
-        acc = msub<false>(acc, L[3], lw2);
-        acc = msub<false>(acc, L[5], lp2);
-        acc = msub<false>(acc, L[6], lp1);
-        acc = msub<false>(acc, L[2], p0);
-        acc = msub<false>(acc, L[4], lw1);
-        acc = msub<false>(acc, L[0], w1);
+struct ChainPart {
+    double acc, t3, t5;
+    __device__ __forceinline__ ChainPart(double r, const double (&L)[7], double w1, double p1, double lw2, double lp2)
+    {
+        if (EXACT) {
+            acc = dsub(dsub(r, dmul(L[0], w1)), dmul(L[1], p1));
+            t3 = dmul(L[3], lw2);
+            t5 = dmul(L[5], lp2);
+        } else {
+            acc = fma(-L[0], w1, fma(-L[5], lp2, fma(-L[3], lw2, fma(-L[1], p1, r))));
+            t3 = t5 = 0.0;
+        }
     }
-    return acc;
-}
-template <bool EXACT>
-__device__ __forceinline__ double bwd_chain(double inv_d, double wf, const double (&Lq)[7], double wb1, double q1,
-                                            double q0, double lw2, double lw1, double lq2, double lq1)
-{
-    double acc = EXACT ? dmul(inv_d, wf) : inv_d * wf;
-    if (EXACT) {  // reference order (_kernels.py:416-428)
-        acc = msub<true>(acc, Lq[0], wb1);
-        acc = msub<true>(acc, Lq[1], q1);
-        acc = msub<true>(acc, Lq[2], q0);
-        acc = msub<true>(acc, Lq[3], lw2);
-        acc = msub<true>(acc, Lq[4], lw1);
-        acc = msub<true>(acc, Lq[5], lq2);
-        acc = msub<true>(acc, Lq[6], lq1);
-    } else {
-        acc = msub<false>(acc, Lq[1], q1);
-        acc = msub<false>(acc, Lq[3], lw2);
-        acc = msub<false>(acc, Lq[5], lq2);
-        acc = msub<false>(acc, Lq[6], lq1);
-        acc = msub<false>(acc, Lq[2], q0);
-        acc = msub<false>(acc, Lq[4], lw1);
-        acc = msub<false>(acc, Lq[0], wb1);
+    __device__ __forceinline__ double finish(const double (&L)[7], double p0, double lw1, double lp1) const
+    {
+        if (EXACT) {
+            double a = dsub(acc, dmul(L[2], p0));
+            a = dsub(a, t3);
+            a = dsub(a, dmul(L[4], lw1));
+            a = dsub(a, t5);
+            return dsub(a, dmul(L[6], lp1));
+        }
+        return fma(-L[4], lw1, fma(-L[2], p0, fma(-L[6], lp1, acc)));
     }
-    return acc;
-}
+};
 
 template <int HELPERS>
 __device__ __forceinline__ void init_smem(Smem &S)
@@ -459,12 +443,25 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                             const long long _s0 = prof ? clock64() : 0;
 #endif
                             const bool p_on = tau <= T1 - 1;
+                            // 1. everything that does not depend on this step's handoff inputs, ahead of
+                            //    the acquire: the ring values, the lane z-1 shuffles of last step's values
+                            //    and the leading part of the substitution
+                            const double2 *r2 = reinterpret_cast<const double2 *>(rg + j * (32 * RS));
+                            const double2 a0 = r2[0], a1 = r2[1], a2 = r2[2], a3 = r2[3];
+                            const double L[7] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x};
+                            const double sw1 = __shfl_up_sync(0xffffffffu, w1, 1);
+                            const double sw2 = __shfl_up_sync(0xffffffffu, w2, 1);
+                            const double sp1 = __shfl_up_sync(0xffffffffu, p1, 1);
+                            const double sp2 = __shfl_up_sync(0xffffffffu, p2, 1);
+                            const double lw2 = gl_on ? ga_prev : sw2;
+                            const double lp2 = gl_on ? gb_prev : sp2;
+                            ChainPart<EXACT> part(a3.y, L, w1, p1, lw2, lp2);
+                            // 2. acquire this step's inputs produced by other warps / CTAs
                             cpa_wait_pd();
                             double *hs = hin + ((tau + 1) & (HR - 1)) * 32;
                             const double *pv = &S.pre[k][tau & (PD - 1)][0][lane];
                             double p0 = p_on ? lds_vol(hs) : 0.0;
                             double ga_cur = gl_ld ? pv[32] : 0.0, gb_cur = gl_ld ? pv[64] : 0.0;
-                            // acquire: inputs produced by other warps / CTAs must be final before the chain
                             bool wt = p_on && (is_sent(p0) || is_sent(ga_cur) || is_sent(gb_cur));
                             if (__builtin_expect(__any_sync(0xffffffffu, wt), 0)) {
                                 long long spins = 0;
@@ -483,19 +480,10 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                                 pc[4] += _s1 - _s0;
                             }
 #endif
-                            double lw1 = __shfl_up_sync(0xffffffffu, w1, 1);
-                            double lw2 = __shfl_up_sync(0xffffffffu, w2, 1);
-                            double lp1 = __shfl_up_sync(0xffffffffu, p1, 1);
-                            double lp2 = __shfl_up_sync(0xffffffffu, p2, 1);
-                            lw1 = gl_on ? ga_cur : lw1;
-                            lw2 = gl_on ? ga_prev : lw2;
-                            lp1 = gl_on ? gb_cur : lp1;
-                            lp2 = gl_on ? gb_prev : lp2;
-                            // the step's seven L values and residual: four 16-byte loads
-                            const double2 *r2 = reinterpret_cast<const double2 *>(rg + j * (32 * RS));
-                            const double2 a0 = r2[0], a1 = r2[1], a2 = r2[2], a3 = r2[3];
-                            const double L[7] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x};
-                            const double acc = fwd_chain<EXACT>(a3.y, L, w1, p1, p0, lw2, lw1, lp2, lp1);
+                            // 3. the rest of the chain: the terms of this step's inputs
+                            const double lw1 = gl_on ? ga_cur : sw1;
+                            const double lp1 = gl_on ? gb_cur : sp1;
+                            const double acc = part.finish(L, p0, lw1, lp1);
                             const bool vpt = tau >= lo && tau <= hi;
                             const double wnew = vpt ? acc : 0.0;
 #ifdef TILU_PLANE_PROF
@@ -587,7 +575,9 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                     for (int m = 0; m < 7; ++m) rg[j * (32 * RS) + m] = isb ? bl[j][m] : d[m][0];
                     if (vpt && !stored) {
 #pragma unroll
+#ifndef TILU_PLANE_NOHELP
                         for (int m = 0; m < 7; ++m) march<K>(d[m]);
+#endif
                     }
                     band_ld(tau + GS, bl[j]);
                 }
@@ -638,7 +628,11 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                     const double *u2 = tb + 2 * (GS + 4) * WIN;  // plane s+1
                     constexpr int Wn = WIN;
                     double res = 0.0;
+#ifndef TILU_PLANE_NOHELP
                     if (sg >= lo && sg <= hi) {
+#else
+                    if (false) {  // experiment: residual helper without arithmetic (results invalid)
+#endif
                         double a[15];
                         if (AMODE == 2) {
                             double hxw[7];
@@ -790,12 +784,27 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                         const int tau = tq - j;
                         if (tau >= T0 - 1) {
                             const bool q_on = tau >= T0;
+                            // 1. ahead of the acquire: ring values (seven source-point L and 1/D), the staged
+                            //    w_f and u of this step, lane z+1's last values, the leading part of the chain
+                            const double2 *r2 = reinterpret_cast<const double2 *>(rg + j * (32 * RS));
+                            const double2 a0 = r2[0], a1 = r2[1], a2 = r2[2], a3 = r2[3];
+                            const double Lq[7] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x};
+                            const double wfv = tb[(GS - 1 - j) * WIN];          // line of tau in the boxes
+                            const double uv = tb[UOFF + (GS - 1 - j) * WIN];
+                            const double sw1 = __shfl_down_sync(0xffffffffu, wb1, 1);
+                            const double sw2 = __shfl_down_sync(0xffffffffu, wb2, 1);
+                            const double sq1 = __shfl_down_sync(0xffffffffu, q1, 1);
+                            const double sq2 = __shfl_down_sync(0xffffffffu, q2, 1);
+                            const double lw2 = gl_on ? ga_prev : sw2;
+                            const double lq2 = gl_on ? gb_prev : sq2;
+                            // reference order (_kernels.py:416-428): inv_d w, then w s se bnw bn bc be sources
+                            ChainPart<EXACT> part(EXACT ? dmul(a3.y, wfv) : a3.y * wfv, Lq, wb1, q1, lw2, lq2);
+                            // 2. acquire this step's inputs produced by other warps / CTAs
                             double q0 = 0.0;
                             cpa_wait_pd();
                             const double *pv = pre + (tau & (PD - 1)) * 96;
                             if (q_on) q0 = gp_on ? (gp_ld ? pv[0] : 0.0) : lds_vol(hin + ((tau - 1) & (HR - 1)) * 32);
                             double ga_cur = gl_ld ? pv[32] : 0.0, gb_cur = gl_ld ? pv[64] : 0.0;
-                            // acquire: inputs produced by other warps must be final before the chain runs
                             if (__any_sync(0xffffffffu,
                                            (q_on && is_sent(q0)) || (gl_ld && (is_sent(ga_cur) || is_sent(gb_cur))))) {
                                 long long spins = 0;
@@ -812,21 +821,10 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
                                     if (++spins > (1ll << 26)) __trap();
                                 }
                             }
-                            double lw1 = __shfl_down_sync(0xffffffffu, wb1, 1);
-                            double lw2 = __shfl_down_sync(0xffffffffu, wb2, 1);
-                            double lq1 = __shfl_down_sync(0xffffffffu, q1, 1);
-                            double lq2 = __shfl_down_sync(0xffffffffu, q2, 1);
-                            lw1 = gl_on ? ga_cur : lw1;
-                            lw2 = gl_on ? ga_prev : lw2;
-                            lq1 = gl_on ? gb_cur : lq1;
-                            lq2 = gl_on ? gb_prev : lq2;
-                            const double wfv = tb[(GS - 1 - j) * WIN];          // line of tau in the boxes
-                            const double uv = tb[UOFF + (GS - 1 - j) * WIN];
-                            double Lq[7];
-#pragma unroll
-                            for (int m = 0; m < 7; ++m) Lq[m] = rg[j * (32 * RS) + m];
-                            const double inv_d = rg[j * (32 * RS) + 7];
-                            const double acc = bwd_chain<EXACT>(inv_d, wfv, Lq, wb1, q1, q0, lw2, lw1, lq2, lq1);
+                            // 3. the terms of this step's inputs
+                            const double lw1 = gl_on ? ga_cur : sw1;
+                            const double lq1 = gl_on ? gb_cur : sq1;
+                            const double acc = part.finish(Lq, q0, lw1, lq1);
                             const bool vpt = tau >= lo && tau <= hi;
                             const double wnew = vpt ? acc : 0.0;
                             if (q_on && k > 0) sts(hin + ((tau - 1) & (HR - 1)) * 32, sentv());
