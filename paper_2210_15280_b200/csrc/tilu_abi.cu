@@ -150,10 +150,10 @@ static int plane_min_level()
 bool batch_ok(const tilu_plan_t *p)
 {
     // packed element offsets are 32-bit: grid * 64 < 2^32 (level <= 9)
-    // the batched kernels compute the residual from the assembled stencil only: plans whose residual
-    // is the operator surrogate (seedA, a_mode='surrogate') take the reference-layout kernels
+    // the batched kernels take the residual from the constant row, per-point rows or the operator
+    // surrogate (seedA); the separable on-the-fly rows (sepk) are plane / reference-layout only
     return !(p->flags & TILU_SCHED_SIMPLE) && p->dev.level <= 9 && p->dev.n >= 4 && p->bsched != nullptr &&
-           p->dev.seedA == nullptr && (p->dev.arow != nullptr || p->dev.arows != nullptr);
+           (p->dev.arow != nullptr || p->dev.arows != nullptr || p->dev.seedA != nullptr);
 }
 
 // Tets per lane of the packed layout (groups of 32 * tpl tets).  More tets per lane amortise the

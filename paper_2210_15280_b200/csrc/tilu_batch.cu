@@ -343,7 +343,38 @@ constexpr size_t ring_smem() { return (size_t)kWarps * D * (8 + (NS * kChunk * 3
 constexpr int kFwdNS = 8;    // forward ring streams: ue us un ubn ubc uts utc f
 constexpr int kBwdNS = 2;    // backward ring streams: w_f(p), u(p)
 
-template <int K, bool EXACT, bool CONST_ROW, int T, bool TAB>
+// Operator-surrogate residual (SurrogateOperator.residual_into, surrogate.py:356-358 ->
+// _kernels.surrogate_apply_residual, _kernels.py:444-483): the 15 stencil weights of a point come from
+// 15 forward-difference tables of the operator surrogate, seeded per row (P.seedA) and marched after
+// every point exactly like the L tables -- shared by the warp (all tets of a batch share the surrogate)
+// and marched lane-parallel in shared memory.  The kx extent is a runtime value (akx1 <= 9).
+__device__ __forceinline__ void smem_march_rt(double *tab, int M, int K, int lane)
+{
+    const int NE = M * (K - 1);
+    if (NE <= 0) return;
+    double nv[(15 * 8 + 31) / 32];
+#pragma unroll
+    for (int i = 0; i < (15 * 8 + 31) / 32; ++i) {
+        const int e = lane + 32 * i;
+        if (e < NE) {
+            const int m = e / (K - 1), j = e - m * (K - 1);
+            nv[i] = dadd(tab[m * K + j], tab[m * K + j + 1]);
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < (15 * 8 + 31) / 32; ++i) {
+        const int e = lane + 32 * i;
+        if (e < NE) {
+            const int m = e / (K - 1), j = e - m * (K - 1);
+            tab[m * K + j] = nv[i];
+        }
+    }
+    __syncwarp();
+}
+
+// AMODE: 0 = per-point rows, 1 = constant row, 3 = operator surrogate (marched weights).
+template <int K, bool EXACT, int AMODE, int T, bool TAB>
 __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_batch_fwd(PlanDev P, BatchArgs A)
 {
     constexpr int GW = 32 * T, D = kStages<T>, NS = kFwdNS, PC = kChunk;
@@ -351,6 +382,7 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_tab[kWarps][7 * K];
     __shared__ double s_L[kWarps][8];
+    __shared__ double s_tabA[AMODE == 3 ? kWarps : 1][AMODE == 3 ? 15 * 9 : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n = P.n;
     const int total = P.nrows * A.G;
     double *tab = s_tab[warp];
@@ -417,6 +449,12 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
         __syncwarp();  // every lane is done with the stages about to be refilled
         for (int c = 0; c < min(D, nch); ++c) issue(c);
         if constexpr (!TAB) smem_load_table<7, K>(tab, P.seedF + (int64_t)R.rid * 7 * K, lane);
+        double *tabA = s_tabA[AMODE == 3 ? warp : 0];
+        if constexpr (AMODE == 3) {
+            const int AK = P.akx1;
+            for (int e = lane; e < 15 * AK; e += 32) tabA[e] = P.seedA[(int64_t)R.rid * 15 * AK + e];
+            __syncwarp();
+        }
         // sliding windows (values of point x-1 / x that point x+1 reuses)
         Vt<T> u_wm = ldv<T>(u + R.oc), u_c = ldv<T>(u + R.oc + GW), us0 = ldv<T>(u + R.os + GW);
         Vt<T> un_m = ldv<T>(u + R.on), ubn_m = ldv<T>(u + R.obn), ubc0 = ldv<T>(u + R.obc + GW);
@@ -447,8 +485,13 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
             nw.bc = ldcgv<T>(wa + R.obc + XN + GW);
             if constexpr (!TAB) fwd_band_load(nband, P, R, z, pn, lane);
             double a[15];
+            if constexpr (AMODE == 3) {
 #pragma unroll
-            for (int i = 0; i < 15; ++i) a[i] = CONST_ROW ? A.arow[i] : P.arows[15 * (int64_t)(R.oc / GW + x) + i];
+                for (int i = 0; i < 15; ++i) a[i] = tabA[i * P.akx1];
+            } else {
+#pragma unroll
+                for (int i = 0; i < 15; ++i) a[i] = AMODE == 1 ? A.arow[i] : P.arows[15 * (int64_t)(R.oc / GW + x) + i];
+            }
             // this point's u/f (and coefficients) from the ring (wait once per chunk)
             const int slot = (x - 1) % PC;
             if (slot == 0) {
@@ -481,23 +524,44 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
             Vt<T> v;
 #pragma unroll
             for (int t = 0; t < T; ++t) {
-                // residual in stencil_apply order (_kernels.py:255-266), then f - A u
-                double acc = EXACT ? dmul(a[7], u_c.a[t]) : a[7] * u_c.a[t];
-                acc = madd<EXACT>(acc, a[0], u_wm.a[t]);
-                acc = madd<EXACT>(acc, a[1], us0.a[t]);
-                acc = madd<EXACT>(acc, a[2], us.a[t]);
-                acc = madd<EXACT>(acc, a[3], ubn_m.a[t]);
-                acc = madd<EXACT>(acc, a[4], ubn.a[t]);
-                acc = madd<EXACT>(acc, a[5], ubc0.a[t]);
-                acc = madd<EXACT>(acc, a[6], ubc.a[t]);
-                acc = madd<EXACT>(acc, a[8], ue.a[t]);
-                acc = madd<EXACT>(acc, a[9], un.a[t]);
-                acc = madd<EXACT>(acc, a[10], un_m.a[t]);
-                acc = madd<EXACT>(acc, a[11], uts.a[t]);
-                acc = madd<EXACT>(acc, a[12], uts0.a[t]);
-                acc = madd<EXACT>(acc, a[13], utc.a[t]);
-                acc = madd<EXACT>(acc, a[14], utc_m.a[t]);
-                const double r = dsub(fv.a[t], acc);
+                double r;
+                if constexpr (AMODE == 3) {
+                    // surrogate_apply_residual order (_kernels.py:470-480): f - c - w s se bnw bn bc be
+                    // - e n nw tse ts tc tw, each product subtracted from the running value
+                    r = msub<EXACT>(fv.a[t], a[7], u_c.a[t]);
+                    r = msub<EXACT>(r, a[0], u_wm.a[t]);
+                    r = msub<EXACT>(r, a[1], us0.a[t]);
+                    r = msub<EXACT>(r, a[2], us.a[t]);
+                    r = msub<EXACT>(r, a[3], ubn_m.a[t]);
+                    r = msub<EXACT>(r, a[4], ubn.a[t]);
+                    r = msub<EXACT>(r, a[5], ubc0.a[t]);
+                    r = msub<EXACT>(r, a[6], ubc.a[t]);
+                    r = msub<EXACT>(r, a[8], ue.a[t]);
+                    r = msub<EXACT>(r, a[9], un.a[t]);
+                    r = msub<EXACT>(r, a[10], un_m.a[t]);
+                    r = msub<EXACT>(r, a[11], uts.a[t]);
+                    r = msub<EXACT>(r, a[12], uts0.a[t]);
+                    r = msub<EXACT>(r, a[13], utc.a[t]);
+                    r = msub<EXACT>(r, a[14], utc_m.a[t]);
+                } else {
+                    // residual in stencil_apply order (_kernels.py:255-266), then f - A u
+                    double acc = EXACT ? dmul(a[7], u_c.a[t]) : a[7] * u_c.a[t];
+                    acc = madd<EXACT>(acc, a[0], u_wm.a[t]);
+                    acc = madd<EXACT>(acc, a[1], us0.a[t]);
+                    acc = madd<EXACT>(acc, a[2], us.a[t]);
+                    acc = madd<EXACT>(acc, a[3], ubn_m.a[t]);
+                    acc = madd<EXACT>(acc, a[4], ubn.a[t]);
+                    acc = madd<EXACT>(acc, a[5], ubc0.a[t]);
+                    acc = madd<EXACT>(acc, a[6], ubc.a[t]);
+                    acc = madd<EXACT>(acc, a[8], ue.a[t]);
+                    acc = madd<EXACT>(acc, a[9], un.a[t]);
+                    acc = madd<EXACT>(acc, a[10], un_m.a[t]);
+                    acc = madd<EXACT>(acc, a[11], uts.a[t]);
+                    acc = madd<EXACT>(acc, a[12], uts0.a[t]);
+                    acc = madd<EXACT>(acc, a[13], utc.a[t]);
+                    acc = madd<EXACT>(acc, a[14], utc_m.a[t]);
+                    r = dsub(fv.a[t], acc);
+                }
                 ss.a[t] = fma(r, r, ss.a[t]);
                 double vv;
                 if (EXACT) {  // reference order: own-row term first (_kernels.py:349-364)
@@ -522,6 +586,7 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_
             st_hand<T>(wa + R.oc + X, v);
             st_sent<T>(wb + R.oc + X, pol_ef);  // re-arm w_b for the backward pass
             if constexpr (!TAB) smem_march<7, K>(tab, lane);
+            if constexpr (AMODE == 3) smem_march_rt(tabA, 15, P.akx1, lane);
             if (slot == PC - 1 || x == m) {  // chunk consumed by every lane: refill its stage
                 __syncwarp();
                 const int c = (x - 1) / PC;
@@ -1020,13 +1085,15 @@ static void launch_fwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_
         A.nwarps = (int)grid * kWarps;
         kern<<<grid, kWarps * 32, sm, s>>>(P, A);
     };
-    const bool c = P.arow != nullptr;
+    const int am = P.seedA ? 3 : P.arow ? 1 : 0;
     if (exact) {
-        if (c) run(k_batch_fwd<K, true, true, T, TAB>);
-        else run(k_batch_fwd<K, true, false, T, TAB>);
+        if (am == 3) run(k_batch_fwd<K, true, 3, T, TAB>);
+        else if (am == 1) run(k_batch_fwd<K, true, 1, T, TAB>);
+        else run(k_batch_fwd<K, true, 0, T, TAB>);
     } else {
-        if (c) run(k_batch_fwd<K, false, true, T, TAB>);
-        else run(k_batch_fwd<K, false, false, T, TAB>);
+        if (am == 3) run(k_batch_fwd<K, false, 3, T, TAB>);
+        else if (am == 1) run(k_batch_fwd<K, false, 1, T, TAB>);
+        else run(k_batch_fwd<K, false, 0, T, TAB>);
     }
 }
 

@@ -75,3 +75,29 @@ def test_batch_shape_mismatch_raises():
         p.pack(u2, ntets=3)
     with pytest.raises(ValueError):
         p.stencil_apply(u2, out=torch.zeros((1, g), dtype=torch.float64, device="cuda"))
+
+
+@pytest.mark.parametrize("level,ntets,fast", [(5, 40, False), (7, 2, False), (6, 3, True)])
+def test_operator_surrogate_batched_kernels(level, ntets, fast):
+    """a_mode='surrogate' through the batched kernels (15 operator-surrogate marchers shared by the
+    warp, surrogate_apply_residual order): bitwise vs the oracle (exact), <= 1e-12 (fast); 40 tets
+    take two-tet lanes (T = 2)."""
+    src = S.stencil_source(lattice.unit_tet(), level, S.sin_kappa())
+    fit = F.fit_surrogate_ilu(src, level, (4, 4, 4), "v1")
+    ac = F.fit_surrogate_operator(src, level, (3, 3, 3))
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, acoefs=ac, fast=fast)
+    u0 = u0_of(level, ntets, seed=7)
+    f = np.zeros_like(u0)
+    f[:, lattice.interior_mask(level)] = 0.25
+    u = cuda(u0)
+    rn = p.sweep(u, cuda(f), 2, norms=True)
+    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows)
+    got = u.cpu().numpy()
+    for t in range(ntets):
+        ref = u0[t].copy()
+        nr = O.sweeps(sur, level, None, ref, f[t], 2, acoefs=ac, return_norms=True)
+        if fast:
+            assert float(np.abs(got[t] - ref).max() / np.abs(ref).max()) <= 1e-12
+        else:
+            assert np.array_equal(got[t], ref)
+        np.testing.assert_allclose(rn.cpu().numpy()[:, t], nr, rtol=1e-10 if fast else 1e-12)
