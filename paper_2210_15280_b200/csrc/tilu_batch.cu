@@ -28,6 +28,8 @@
 // Every load of point x+1 is issued while point x computes (one-point software prefetch).
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 #include "tilu_batch.cuh"
 #include "tilu_common.cuh"
@@ -1058,7 +1060,31 @@ void launch_arm(const PlanDev &P, double *wa, const unsigned long long *hdr, uns
 }
 
 // Persistent grid: as many CTAs as fit on the device at once (queried once per kernel).
-constexpr int kMaxDevices = 64;
+template <class Kern>
+static unsigned persistent_grid(Kern k, size_t smem);
+
+// Launch a persistent batched kernel.  Its dynamic shared-memory attribute and resident grid are
+// cached per KERNEL and per device ordinal (a map keyed by the kernel's address: kernels of one
+// signature share a C++ type, so a per-type static would skip the attribute of the second one).
+template <class Kern>
+static void launch_persistent(Kern kern, size_t sm, const PlanDev &P, BatchArgs A, cudaStream_t s)
+{
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, unsigned> grids;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    unsigned grid;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto key = std::make_pair(reinterpret_cast<const void *>(kern), dev);
+        auto it = grids.find(key);
+        if (it == grids.end()) it = grids.emplace(key, persistent_grid(kern, sm)).first;
+        grid = it->second;
+    }
+    A.nwarps = (int)grid * kWarps;
+    kern<<<grid, kWarps * 32, sm, s>>>(P, A);
+}
+
 template <class Kern>
 static unsigned persistent_grid(Kern k, size_t smem)
 {
@@ -1074,17 +1100,7 @@ template <int K, int T, bool TAB>
 static void launch_fwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_t s)
 {
     constexpr size_t sm = ring_smem<kFwdNS, T, kStages<T>>();
-    auto run = [&](auto kern) {
-        // the smem attribute and the resident grid are per device: cached per device ordinal
-        static unsigned grids[kMaxDevices] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev < 0 || dev >= kMaxDevices) dev = 0;
-        if (!grids[dev]) grids[dev] = persistent_grid(kern, sm);
-        const unsigned grid = grids[dev];
-        A.nwarps = (int)grid * kWarps;
-        kern<<<grid, kWarps * 32, sm, s>>>(P, A);
-    };
+    auto run = [&](auto kern) { launch_persistent<decltype(kern)>(kern, sm, P, A, s); };
     const int am = P.seedA ? 3 : P.arow ? 1 : 0;
     if (exact) {
         if (am == 3) run(k_batch_fwd<K, true, 3, T, TAB>);
@@ -1101,17 +1117,7 @@ template <int K, int T, bool TAB>
 static void launch_bwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_t s)
 {
     constexpr size_t sm = ring_smem<kBwdNS, T, kStages<T>>();
-    auto run = [&](auto kern) {
-        // the smem attribute and the resident grid are per device: cached per device ordinal
-        static unsigned grids[kMaxDevices] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev < 0 || dev >= kMaxDevices) dev = 0;
-        if (!grids[dev]) grids[dev] = persistent_grid(kern, sm);
-        const unsigned grid = grids[dev];
-        A.nwarps = (int)grid * kWarps;
-        kern<<<grid, kWarps * 32, sm, s>>>(P, A);
-    };
+    auto run = [&](auto kern) { launch_persistent<decltype(kern)>(kern, sm, P, A, s); };
     if (exact) run(k_batch_bwd<K, true, T, TAB>);
     else run(k_batch_bwd<K, false, T, TAB>);
 }
