@@ -73,6 +73,8 @@ typedef struct {
        NULL: not used. */
     const double *sepk_tables;
     double sepk_c0, sepk_w;
+    const double *factors_dev;  /* DEVICE [grid][9] CellILU rows, e.g. written by tilu_factorize_device (used
+                                   when `factors` is NULL; caller-owned, must outlive the plan), or NULL */
 } tilu_desc_t;
 
 /* Build a device plan: uploads coefficients, band rows and stencil, precomputes the
@@ -142,6 +144,31 @@ int tilu_stored_sweep(const tilu_plan_t *plan, double *u, const double *f, int n
 int64_t tilu_factorize_stream(int n, const int64_t *rowoff, const double *arows, int aconst,
                               double *full_store, int do_full, const int64_t *collect_ranks,
                               int64_t ncollect, double *collect_out, double pivot_eps);
+
+/* On-device streaming factorization: the same factorization as tilu_factorize_stream
+ * (_kernels.factorize_stream, _kernels.py:39-143; factorize_tet ilu.py:139-175 with full_store=True),
+ * computed by a hyperplane-wavefront kernel, bitwise equal to the host routine.  Exactly one operator
+ * source: arows_dev (DEVICE [grid][15] per-point rows), arow (HOST [15] constant row) or
+ * sepk_tables_dev (DEVICE [3][4n+1], config 3's separable coefficient evaluated on the fly).
+ * store_dev: DEVICE [grid][9] factor rows (L_w..L_be, D, 1/D; ilu.py:32), interior rows written, the
+ * rest untouched.  *status_host = 0, or 1 + rank of the first vanishing pivot (|D| < pivot_eps; the
+ * call then returns TILU_EPIVOT).  Synchronises `stream` before returning. */
+int tilu_factorize_device(int level, const double *arows_dev, const double *arow, const double *sepk_tables_dev,
+                          double sepk_c0, double sepk_w, double *store_dev, double pivot_eps,
+                          int64_t *status_host, void *stream);
+/* out_dev[i][0..8] = store_dev[ranks_dev[i]][0..8]: the sampled / band rows the fit and the V1 store
+ * take from the factorization (factorize_stream's collect_ranks / collect_out).  DEVICE pointers. */
+int tilu_gather_rows(const double *store_dev, const int64_t *ranks_dev, int64_t count, double *out_dev,
+                     void *stream);
+
+/* Multigrid transfers on one macro-tet lattice, vectors in the reference layout, DEVICE:
+ * r_coarse = P^T r_fine on interior coarse points, 0 elsewhere (Hierarchy.restrict / v_cycle,
+ * multigrid.py:383-388, 476-480; P = build_prolongation, multigrid.py:241-277; the fine level is
+ * coarse_level + 1, r_fine zero outside its interior); u_fine += P e_coarse on interior fine points
+ * (multigrid.py:482); y = M x for the coarsest-level inverse (Hierarchy.coarse_solve, :445-457). */
+int tilu_mg_restrict(int coarse_level, const double *r_fine, double *r_coarse, void *stream);
+int tilu_mg_prolong_add(int coarse_level, const double *e_coarse, double *u_fine, void *stream);
+int tilu_dense_mv(int m, const double *M, const double *x, double *y, void *stream);
 
 /* Host-side setup: rows [grid][15] (interior rows written, others untouched) of a separable scalar
  * coefficient on the unit macro-tet from its [3][4n+1] tables -- bitwise the reference's per-point

@@ -36,6 +36,7 @@ class TiluDesc(ctypes.Structure):
         ("lcoefs", _P), ("dcoefs", _P), ("band_ranks", _P), ("nband", _L), ("store_rows", _P),
         ("arow", _P), ("arows_dev", _P), ("acoefs", _P), ("akx1", _I), ("aky1", _I), ("akz1", _I),
         ("factors", _P), ("flags", _I), ("sepk_tables", _P), ("sepk_c0", _D), ("sepk_w", _D),
+        ("factors_dev", _P),
     ]
 
 
@@ -48,6 +49,7 @@ EXPORTS = (
     "tilu_profile_enable", "tilu_profile_reset", "tilu_profile_read", "tilu_packed_size",
     "tilu_packed_scratch_size", "tilu_pack",
     "tilu_unpack", "tilu_sweep_packed", "tilu_plane_tasks", "tilu_sepk_rows",
+    "tilu_factorize_device", "tilu_gather_rows", "tilu_mg_restrict", "tilu_mg_prolong_add", "tilu_dense_mv",
 )
 
 
@@ -93,6 +95,16 @@ def lib():
     L.tilu_sweep_packed.restype = _I
     L.tilu_sepk_rows.argtypes = [_I, _P, _D, _D, _P]
     L.tilu_sepk_rows.restype = _I
+    L.tilu_factorize_device.argtypes = [_I, _P, _P, _P, _D, _D, _P, _D, _P, _P]
+    L.tilu_factorize_device.restype = _I
+    L.tilu_gather_rows.argtypes = [_P, _P, _L, _P, _P]
+    L.tilu_gather_rows.restype = _I
+    L.tilu_mg_restrict.argtypes = [_I, _P, _P, _P]
+    L.tilu_mg_restrict.restype = _I
+    L.tilu_mg_prolong_add.argtypes = [_I, _P, _P, _P]
+    L.tilu_mg_prolong_add.restype = _I
+    L.tilu_dense_mv.argtypes = [_I, _P, _P, _P, _P]
+    L.tilu_dense_mv.restype = _I
     L.tilu_plane_tasks.argtypes = [_I, _P, _I]
     L.tilu_plane_tasks.restype = _I
     L.tilu_profile_enable.argtypes = [_I]

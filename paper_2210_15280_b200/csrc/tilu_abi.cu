@@ -92,6 +92,22 @@ int fail(int code, const char *fmt, ...)
     return code;
 }
 
+}  // namespace
+
+// error / launch accounting for the other translation units of the ABI (tilu_factor.cu, tilu_mg.cu)
+namespace tilu {
+int abi_fail(int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+void abi_count_launches(int k) { g_launches = k; }
+}  // namespace tilu
+
+namespace {
 int check_cuda(const char *what)
 {
     cudaError_t e = cudaGetLastError();
@@ -472,7 +488,7 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
     // one operator form: on-the-fly separable rows, else the constant row, else per-point rows
     P.arow = dsepk ? nullptr : darow;
     P.arows = (dsepk || d->arow) ? nullptr : d->arows_dev;
-    P.factors = dfactors;
+    P.factors = dfactors ? dfactors : d->factors_dev;
     if (d->acoefs) {
         P.akx1 = d->akx1;
         p->ky1a = d->aky1;

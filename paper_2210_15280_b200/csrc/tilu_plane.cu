@@ -968,6 +968,13 @@ __global__ void __launch_bounds__(2 * PW * 32, 1) k_plane_bwd(const PlanDev P, c
     }
 }
 
+// Experimental one-warp-per-diagonal variant (no helper warps).  Bitwise equal, but measured slower at
+// every level (L9 forward 1.82 ms vs 1.02 ms: one warp per scheduler partition hides no latency), so it
+// is only compiled with -DTILU_PLANE_FUSED_BUILD and selected with TILU_PLANE_FUSED=1.
+#ifdef TILU_PLANE_FUSED_BUILD
+#include "tilu_plane_fused.cuh"
+#endif
+
 // ------------------------------------------------------------------------------------------------
 // Layout conversion, arming, norms.
 // ------------------------------------------------------------------------------------------------
@@ -1055,6 +1062,9 @@ struct Workspace {
     long long *trace = nullptr;  // [2][ntasks][4] (TILU_PLANE_TRACE)
     long long *steplog = nullptr;
     Maps maps;
+#ifdef TILU_PLANE_FUSED_BUILD
+    MapsF mapsf;
+#endif
 };
 
 // TMA tensor map over one plane-layout vector: dims (ZP, TP, n+1), box (WIN, box_tau, box_s).
@@ -1151,6 +1161,53 @@ static bool launch_pass(const PlanDev &P, const Args &A, const Maps &M, int ctas
          : am == 1 ? launch_e<false, 1>(P, A, M, ctas, fwd, s) : launch_e<false, 0>(P, A, M, ctas, fwd, s);
 }
 
+#ifdef TILU_PLANE_FUSED_BUILD
+// Fused kernels (tilu_plane_fused.cuh): constant row or separable-coefficient rows, no stored factors.
+template <int K, bool EXACT, int AMODE>
+static bool launchf_k(const PlanDev &P, const Args &A, const MapsF &M, int ctas, bool fwd, cudaStream_t s)
+{
+    static signed char attrs[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!attrs[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(k_planef_fwd<K, EXACT, AMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(SmemF));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_planef_bwd<K, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemF));
+        attrs[dev] = (e == cudaSuccess) ? 1 : -1;
+    }
+    if (attrs[dev] < 0) return false;
+    if (fwd) k_planef_fwd<K, EXACT, AMODE><<<ctas, PW * 32, sizeof(SmemF), s>>>(P, A, M);
+    else k_planef_bwd<K, EXACT><<<ctas, PW * 32, sizeof(SmemF), s>>>(P, A, M);
+    return true;
+}
+template <bool EXACT, int AMODE>
+static bool launchf_e(const PlanDev &P, const Args &A, const MapsF &M, int ctas, bool fwd, cudaStream_t s)
+{
+    switch (P.kx1) {
+    case 1: return launchf_k<1, EXACT, AMODE>(P, A, M, ctas, fwd, s);
+    case 2: return launchf_k<2, EXACT, AMODE>(P, A, M, ctas, fwd, s);
+    case 3: return launchf_k<3, EXACT, AMODE>(P, A, M, ctas, fwd, s);
+    case 4: return launchf_k<4, EXACT, AMODE>(P, A, M, ctas, fwd, s);
+    case 5: return launchf_k<5, EXACT, AMODE>(P, A, M, ctas, fwd, s);
+    case 6: return launchf_k<6, EXACT, AMODE>(P, A, M, ctas, fwd, s);
+    default: return false;
+    }
+}
+static bool fused_ok(const PlanDev &P, bool stored)
+{
+    static const char *e = std::getenv("TILU_PLANE_FUSED");
+    if (!e || e[0] != '1') return false;
+    return !stored && (P.sepk || P.arow);
+}
+static bool launchf_pass(const PlanDev &P, const Args &A, const MapsF &M, int ctas, bool exact, bool fwd, cudaStream_t s)
+{
+    if (P.sepk) return exact ? launchf_e<true, 2>(P, A, M, ctas, fwd, s) : launchf_e<false, 2>(P, A, M, ctas, fwd, s);
+    return exact ? launchf_e<true, 1>(P, A, M, ctas, fwd, s) : launchf_e<false, 1>(P, A, M, ctas, fwd, s);
+}
+#endif
+
 static int resident_ctas(const tilu_plan *p)
 {
     int dev = 0, sms = 148;
@@ -1200,6 +1257,16 @@ static int ws_create(tilu_plan *p, Workspace **out, cudaStream_t s)
         delete w;
         return TILU_ECUDA;
     }
+#ifdef TILU_PLANE_FUSED_BUILD
+    if (!encode_map(&w->mapsf.u3g, w->u, w->g, GS, 3)) {
+        cudaFree(m);
+        delete w;
+        return TILU_ECUDA;
+    }
+    w->mapsf.f1 = w->maps.f1;
+    w->mapsf.w1 = w->maps.w1;
+    w->mapsf.u1 = w->maps.u1;
+#endif
     if (cudaStreamSynchronize(s) != cudaSuccess || cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming) != cudaSuccess) {
         cudaFree(m);
         delete w;
@@ -1279,8 +1346,8 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
     if (trace_path && !w->trace) cudaMalloc(&w->trace, 2 * (size_t)w->ntasks * TR * sizeof(long long));
     static const char *steplog_path = std::getenv("TILU_PLANE_STEPLOG");
     if (steplog_path && !w->steplog) {
-        cudaMalloc(&w->steplog, 3 * PW * 8 * sizeof(long long));
-        cudaMemset(w->steplog, 0, 3 * PW * 8 * sizeof(long long));
+        cudaMalloc(&w->steplog, 2 * 3 * PW * 8 * sizeof(long long));
+        cudaMemset(w->steplog, 0, 2 * 3 * PW * 8 * sizeof(long long));
     }
     prof_begin(s);
     launch_xpose(P, w->g, u, w->u, false, s);
@@ -1303,12 +1370,18 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
             A.prof_task = pt ? std::atoi(pt) : 0;
         }
         prof_begin(s);
+#ifdef TILU_PLANE_FUSED_BUILD
+        const bool fused = fused_ok(P, stored);
+        bool ok = fused ? launchf_pass(P, A, w->mapsf, w->ctas, exact, true, s)
+                        : launch_pass(P, A, w->maps, w->ctas, exact, true, s);
+#else
         bool ok = launch_pass(P, A, w->maps, w->ctas, exact, true, s);
+#endif
         prof_end("plane_fwd", s);
         A.ticket = w->ticket + 1;
         A.part = nullptr;
         A.trace = w->trace ? w->trace + (size_t)w->ntasks * TR : nullptr;
-        A.steplog = nullptr;
+        A.steplog = w->steplog ? w->steplog + 3 * PW * 8 : nullptr;
         static const char *dbg = std::getenv("TILU_PLANE_DEBUG");  // "1": forward pass only, return w_f
         if (dbg && dbg[0] == '1') {
             launch_xpose(P, w->g, w->W, u, true, s);
@@ -1317,7 +1390,12 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
             return ok ? TILU_OK : TILU_EUNSUPPORTED;
         }
         prof_begin(s);
+#ifdef TILU_PLANE_FUSED_BUILD
+        ok = ok && (fused ? launchf_pass(P, A, w->mapsf, w->ctas, exact, false, s)
+                          : launch_pass(P, A, w->maps, w->ctas, exact, false, s));
+#else
         ok = ok && launch_pass(P, A, w->maps, w->ctas, exact, false, s);
+#endif
         prof_end("plane_bwd", s);
         nl += 2;
         if (!ok) rc = TILU_EUNSUPPORTED;
@@ -1327,11 +1405,11 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
         }
     }
     if (steplog_path && w->steplog) {
-        std::vector<long long> h(3 * PW * 8);
+        std::vector<long long> h(2 * 3 * PW * 8);
         cudaMemcpy(h.data(), w->steplog, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
         if (FILE *fp = std::fopen(steplog_path, "w")) {
-            std::fprintf(fp, "warp total armed ringwait tmawait acquire groups chain tail\n");
-            for (int wv = 0; wv < 3 * PW; ++wv) {
+            std::fprintf(fp, "warp total armed ringwait tmawait acquire groups chain tail  (fused: total armed tma cpwait acquire plain - groups; rows 12.. = backward)\n");
+            for (int wv = 0; wv < 2 * 3 * PW; ++wv) {
                 std::fprintf(fp, "%d", wv);
                 for (int i = 0; i < 8; ++i) std::fprintf(fp, " %lld", h[wv * 8 + i]);
                 std::fprintf(fp, "\n");

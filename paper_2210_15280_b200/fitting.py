@@ -206,6 +206,11 @@ class FactorizationResult:
 
 
 def _pivot_eps(source: StencilSource) -> float:
+    if source.data is None and source.sepk is not None:
+        # table-form source without materialised rows: bound of the centre entry (<= 24 k W)
+        t = np.abs(np.asarray(source.sepk.tables))
+        kmax = abs(float(source.sepk.c0)) + float(t[0].max() * t[1].max() * t[2].max())
+        return 1e-300 * max(24.0 * kmax * float(source.sepk.w), 1.0)
     data = np.atleast_2d(source.data)
     scale = abs(float(data[0, lattice.C])) if source.constant else float(np.abs(data[:, lattice.C]).max())
     return 1e-300 * max(scale, 1.0)
@@ -229,6 +234,56 @@ def factorize_tet(source: StencilSource, level: int, *, full_store: bool = True,
     tri = (n + 1) * (n + 2) // 2
     return FactorizationResult(level, rows if full_store else None, collected if len(cr) else None,
                                2 * tri * 8 * 8 + collected.nbytes, rows.nbytes if full_store else 0)
+
+
+def factorize_tet_device(source: StencilSource, level: int, *, full_store: bool = True, collect_ranks=None,
+                         device="cuda", keep_on_device: bool = False) -> FactorizationResult:
+    """The same factorization on the GPU (``tilu_factorize_device``: hyperplane-wavefront kernel, bitwise
+    equal to ``factorize_tet`` / the reference's ``factorize_stream``).  The operator comes from the
+    source's cheapest form: the separable-coefficient tables (config 3: rows evaluated on the fly, no
+    [grid, 15] array), the constant row, or the per-point rows (uploaded).  ``collect_ranks`` rows are
+    gathered on the device and returned as a host array; the full store is returned as a host array, or
+    as the CUDA tensor itself with ``keep_on_device`` (for ``DevicePlan(factors=...)``)."""
+    import torch
+
+    L = _lib.lib()
+    dev = torch.device(device)
+    grid = lattice.grid_size(level)
+    with torch.cuda.device(dev):
+        store = torch.zeros((grid, 9), dtype=torch.float64, device=dev)
+        status = ctypes.c_int64(0)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        rows_dev = tab_dev = None
+        arow = None
+        c0 = w = 0.0
+        if getattr(source, "sepk", None) is not None:
+            tab_dev = torch.as_tensor(np.ascontiguousarray(source.sepk.tables, dtype=np.float64), device=dev)
+            c0, w = float(source.sepk.c0), float(source.sepk.w)
+        elif source.constant:
+            arow = np.ascontiguousarray(np.atleast_1d(source.data), dtype=np.float64).reshape(15)
+        else:
+            data = source.data
+            rows_dev = (data if isinstance(data, torch.Tensor) else
+                        torch.as_tensor(np.ascontiguousarray(data, dtype=np.float64), device=dev)).contiguous()
+        rc = L.tilu_factorize_device(
+            level, rows_dev.data_ptr() if rows_dev is not None else None,
+            arow.ctypes.data if arow is not None else None,
+            tab_dev.data_ptr() if tab_dev is not None else None, ctypes.c_double(c0), ctypes.c_double(w),
+            store.data_ptr(), ctypes.c_double(_pivot_eps(source)), ctypes.byref(status), stream)
+        if rc == _lib.TILU_EPIVOT:
+            raise PivotBreakdown(lattice.lattice_coords(level)[status.value - 1])
+        _lib.check(rc)
+        collected = None
+        if collect_ranks is not None and len(collect_ranks):
+            cr = torch.as_tensor(np.ascontiguousarray(collect_ranks, dtype=np.int64), device=dev)
+            out = torch.empty((len(cr), 9), dtype=torch.float64, device=dev)
+            _lib.check(L.tilu_gather_rows(store.data_ptr(), cr.data_ptr(), len(cr), out.data_ptr(), stream))
+            collected = out.cpu().numpy()
+        rows = None
+        if full_store:
+            rows = store if keep_on_device else store.cpu().numpy()
+    return FactorizationResult(level, rows, collected, 0 if collected is None else collected.nbytes,
+                               grid * 72 if full_store else 0)
 
 
 # ------------------------------------------------------------------------------------------
@@ -259,7 +314,11 @@ class SurrogateFit:
 
 
 def fit_surrogate_ilu(source: StencilSource, level: int, degrees, variant: str = "v1",
-                      sample_level=None) -> SurrogateFit:
+                      sample_level=None, factorize: str = "host") -> SurrogateFit:
+    """``factorize``: "host" (native two-layer sweep on the CPU) or "device" (the wavefront kernel on the
+    GPU; same factor rows bitwise, so the fit is identical)."""
+    if factorize not in ("host", "device"):
+        raise ValueError(f"unknown factorize mode {factorize!r}")
     if variant not in ("v1", "v2"):
         raise ValueError(f"unknown variant {variant!r}")
     degrees = tuple(int(d) for d in degrees)
@@ -278,7 +337,8 @@ def fit_surrogate_ilu(source: StencilSource, level: int, degrees, variant: str =
             eff = supported_degrees([sets[d] for d in targets], degrees)
             ranks = [lattice.lattice_rank(c, level) for c in sets.values() if len(c)]
             union = np.unique(np.concatenate(ranks + [band]))
-            res = factorize_tet(source, level, full_store=False, collect_ranks=union)
+            res = (factorize_tet_device if factorize == "device" else factorize_tet)(
+                source, level, full_store=False, collect_ranks=union)
             rows = res.collected
 
             def fit_all(deg, sets=sets, union=union, rows=rows):

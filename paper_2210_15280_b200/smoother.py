@@ -101,7 +101,13 @@ class DevicePlan:
             ac = _f64(acoefs)
             d.acoefs = self._ptr(ac)
             d.akx1, d.aky1, d.akz1 = ac.shape[1:]
-        if factors is not None:
+        if isinstance(factors, torch.Tensor) and factors.is_cuda:
+            # device-resident factor store (fitting.factorize_tet_device): used in place, no upload
+            if factors.dtype != torch.float64 or not factors.is_contiguous():
+                raise ValueError("device factors must be a contiguous float64 tensor [grid, 9]")
+            self._factors = factors
+            d.factors_dev = factors.data_ptr()
+        elif factors is not None:
             d.factors = self._ptr(_f64(factors))
         if sepk is not None:
             if int(sepk.level) != self.level:
@@ -286,10 +292,11 @@ class SurrogateILU(fitting.SurrogateFit):
 
 
 def build_surrogate_ilu(source: StencilSource, level: int, degrees, variant: str = "v1",
-                        sample_level=None, fast: bool = False) -> SurrogateILU:
-    """Host setup (streaming factorization + LSQ fit) of a device surrogate ILU(0)
-    (reference surrogate.py:266-326)."""
-    return SurrogateILU(fitting.fit_surrogate_ilu(source, level, degrees, variant, sample_level), fast)
+                        sample_level=None, fast: bool = False, factorize: str = "host") -> SurrogateILU:
+    """Setup (streaming factorization + LSQ fit) of a device surrogate ILU(0) (reference
+    surrogate.py:266-326); ``factorize="device"`` runs the factorization sweep on the GPU (same rows
+    bitwise), the least-squares fit stays on the host."""
+    return SurrogateILU(fitting.fit_surrogate_ilu(source, level, degrees, variant, sample_level, factorize), fast)
 
 
 class CellILU:
@@ -342,7 +349,7 @@ class SurrogateILUSmoother:
     (multigrid.py:414-429) on the GPU."""
 
     def __init__(self, source: StencilSource, level: int, config: SmootherConfig, fast: bool = False,
-                 simple: bool = False):
+                 simple: bool = False, factorize: str = "host"):
         self.source = source
         self.level = level
         self.config = config
@@ -359,29 +366,32 @@ class SurrogateILUSmoother:
         else:
             op["arows"] = source.data
         if config.kind == "ilu":
-            self.factorization = fitting.factorize_tet(source, level)
+            self.factorization = (fitting.factorize_tet_device(source, level, keep_on_device=True)
+                                  if factorize == "device" else fitting.factorize_tet(source, level))
             self.precond = CellILU(self.factorization)
             self.plan = DevicePlan(level, np.zeros((7, 1, 1, 1)), np.zeros(1), "v2",
                                    factors=self.factorization.rows, fast=fast, simple=simple, **op)
             self._stored = True
         else:
             self.precond = build_surrogate_ilu(source, level, config.degrees, config.variant,
-                                               config.sample_level, fast=fast)
+                                               config.sample_level, fast=fast, factorize=factorize)
             self.plan = self.precond.plan(simple=simple, **op)
             self._stored = False
 
     @classmethod
     def setup(cls, source, level: int | None = None, degrees=(3, 3, 3), variant: str = "v1",
               sample_level=None, *, coeff: CoefficientField | None = None, kind: str = "surrogate_ilu",
-              a_mode: str = "assembled", a_degrees=(3, 3, 3), fast: bool = False, simple: bool = False):
-        """``source`` is a StencilSource, or macro-tet vertices (4, 3) plus ``coeff``."""
+              a_mode: str = "assembled", a_degrees=(3, 3, 3), fast: bool = False, simple: bool = False,
+              factorize: str = "host"):
+        """``source`` is a StencilSource, or macro-tet vertices (4, 3) plus ``coeff``.  ``factorize``:
+        where the ILU(0) factorization sweep of the setup runs ("host" or "device", same rows bitwise)."""
         if not isinstance(source, StencilSource):
             if level is None:
                 raise ValueError("level is required when passing vertices")
             source = stencil_source(source, level, coeff or CoefficientField.constant(1.0))
         level = source.level if level is None else level
         cfg = SmootherConfig(kind, tuple(degrees), variant, sample_level, a_mode, tuple(a_degrees))
-        return cls(source, level, cfg, fast=fast, simple=simple)
+        return cls(source, level, cfg, fast=fast, simple=simple, factorize=factorize)
 
     @property
     def degrees(self):

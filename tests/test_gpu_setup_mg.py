@@ -1,0 +1,181 @@
+"""SURVEY 8(f)3 and 8(f)2 on the GPU:
+* the on-device streaming factorization (tilu_factorize_device) equals the host routine and the
+  reference's factorize_tet rows bitwise (constant, per-point and on-the-fly separable rows), reports
+  the reference's first vanishing pivot, and feeds an identical surrogate fit / stored-factor smoother;
+* the multigrid transfers are bitwise the reference's P^T r / P e (golden vectors from the live
+  reference and the numpy restatement at other levels), and the V-cycle and its convergence factor
+  match the reference Hierarchy (tolerances stated at the asserts)."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import GOLDEN  # noqa: E402
+from oracle import mg_oracle as MO  # noqa: E402
+from paper_2210_15280_b200 import SmootherConfig, SurrogateILUSmoother, lattice  # noqa: E402
+from paper_2210_15280_b200 import fitting as F  # noqa: E402
+from paper_2210_15280_b200 import multigrid as MG  # noqa: E402
+from paper_2210_15280_b200 import stencil as S  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def cuda(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+
+
+SOURCES = {
+    "const": lambda L: S.stencil_source(lattice.unit_tet(), L, S.CoefficientField.constant(1.0)),
+    "tensor": lambda L: S.stencil_source(lattice.distorted_tet(), L, S.diag_tensor((1, 1, 1e-3))),
+    "sepk": lambda L: S.stencil_source(lattice.unit_tet(), L, S.sin_kappa()),
+}
+
+
+@pytest.mark.parametrize("kind,level", [("const", 2), ("const", 3), ("const", 5), ("tensor", 4), ("tensor", 6),
+                                        ("sepk", 3), ("sepk", 5), ("sepk", 6), ("const", 7), ("sepk", 7)])
+def test_device_factorization_bitwise_vs_host(kind, level):
+    src = SOURCES[kind](level)
+    band = lattice.band_ranks(level)
+    host = F.factorize_tet(src, level, full_store=True, collect_ranks=band)
+    dev = F.factorize_tet_device(src, level, full_store=True, collect_ranks=band)
+    assert np.array_equal(dev.rows, host.rows)
+    if len(band):
+        assert np.array_equal(dev.collected, host.collected)
+
+
+CFG_COEFF = {
+    "cfg1": lambda: S.CoefficientField.constant(1.0),
+    "cfg2": lambda: S.diag_tensor((1, 1, 1e-3)),
+    "cfg3": S.sin_kappa,
+    "cfg4": lambda: S.CoefficientField.constant(1.0),
+    "cfg5": lambda: S.diag_tensor((1, 1e-2, 1)),
+}
+
+
+def test_device_factorization_vs_reference_golden():
+    cases = [p for p in sorted(glob.glob(os.path.join(GOLDEN, "cfg*.npz"))) if "factors" in np.load(p).files]
+    assert cases
+    for p in cases:
+        d = np.load(p)
+        level = int(d["level"])
+        src = S.stencil_source(d["verts"], level, CFG_COEFF[os.path.basename(p)[:4]]())
+        dev = F.factorize_tet_device(src, level)
+        assert np.array_equal(dev.rows, d["factors"]), os.path.basename(p)
+
+
+def test_device_factorization_pivot_breakdown_matches_host():
+    level = 4
+    src = SOURCES["tensor"](level)
+    data = src.data.copy()
+    inner = lattice.lattice_coords(level, "interior")
+    bad = lattice.lattice_rank(inner[[37, 120]], level)
+    data[bad] = 0.0          # two vanishing pivots: the first in (z, y, x) order must be reported
+    broken = S.StencilSource(level, data, False)
+    with pytest.raises(F.PivotBreakdown) as eh:
+        F.factorize_tet(broken, level)
+    with pytest.raises(F.PivotBreakdown) as ed:
+        F.factorize_tet_device(broken, level)
+    assert str(eh.value) == str(ed.value)
+
+
+@pytest.mark.parametrize("kind,level,q", [("const", 5, 4), ("tensor", 5, 3), ("sepk", 6, 4)])
+def test_fit_with_device_factorization_is_identical(kind, level, q):
+    src = SOURCES[kind](level)
+    a = F.fit_surrogate_ilu(src, level, (q, q, q), "v1")
+    b = F.fit_surrogate_ilu(src, level, (q, q, q), "v1", factorize="device")
+    assert a.degrees == b.degrees and a.stride == b.stride
+    assert np.array_equal(a.lcoefs, b.lcoefs) and np.array_equal(a.dcoefs, b.dcoefs)
+    assert np.array_equal(a.store_rows, b.store_rows) and np.array_equal(a.band_ranks, b.band_ranks)
+
+
+def test_stored_ilu_smoother_on_device_factors():
+    level = 6
+    mask = lattice.interior_mask(level)
+    u0 = np.zeros(lattice.grid_size(level))
+    u0[mask] = np.random.default_rng(5).uniform(-1, 1, int(mask.sum()))
+    f = np.zeros_like(u0)
+    outs = []
+    for mode in ("host", "device"):
+        sm = SurrogateILUSmoother.setup(lattice.distorted_tet(), level, coeff=S.diag_tensor((1, 1e-2, 1)), kind="ilu",
+                                        factorize=mode)
+        u = cuda(u0)
+        sm.apply(u, cuda(f), 3)
+        outs.append(u.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+
+
+# ---- multigrid (8(f)2) -----------------------------------------------------------------------
+
+MG_CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "mg_*.npz")))
+COEFF = {"mg_unit_L5_surr": lambda: S.CoefficientField.constant(1.0),
+         "mg_unit_L5_ilu": lambda: S.CoefficientField.constant(1.0),
+         "mg_dist_L5_surr": lambda: S.diag_tensor((1, 1, 1e-1))}
+
+
+def hierarchy(d, name):
+    cfg = SmootherConfig(kind=str(d["kind"]), degrees=tuple(int(v) for v in d["degrees"]), variant=str(d["variant"]))
+    return MG.Hierarchy(d["verts"], int(d["lmin"]), int(d["lmax"]), COEFF[name](), cfg, int(d["nu"]), int(d["nu"]))
+
+
+@pytest.mark.parametrize("name", MG_CASES)
+def test_transfers_bitwise_vs_reference(name):
+    d = np.load(os.path.join(GOLDEN, name + ".npz"))
+    H = hierarchy(d, name)
+    top = H.top
+    rc = H.restrict(top, cuda(d["xfer_r"]))
+    assert np.array_equal(rc.cpu().numpy(), d["xfer_rc"])
+    u = H.zero(top)
+    H.prolongate_add(top, cuda(d["xfer_e"]), u)
+    assert np.array_equal(u.cpu().numpy(), d["xfer_pe"])
+
+
+@pytest.mark.parametrize("coarse_level", [1, 2, 5, 6])
+def test_transfers_bitwise_vs_restatement(coarse_level):
+    lf = coarse_level + 1
+    rng = np.random.default_rng(coarse_level)
+    r = np.where(lattice.interior_mask(lf), rng.standard_normal(lattice.grid_size(lf)), 0.0)
+    e = np.where(lattice.interior_mask(coarse_level), rng.standard_normal(lattice.grid_size(coarse_level)), 0.0) \
+        if coarse_level >= 2 else np.zeros(lattice.grid_size(coarse_level))
+    from paper_2210_15280_b200 import _lib
+    import ctypes
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    rc = torch.zeros(lattice.grid_size(coarse_level), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().tilu_mg_restrict(coarse_level, cuda(r).data_ptr(), rc.data_ptr(), st))
+    assert np.array_equal(rc.cpu().numpy(), MO.restrict(r, coarse_level))
+    u0 = np.where(lattice.interior_mask(lf), rng.standard_normal(lattice.grid_size(lf)), 0.0)
+    u = cuda(u0)
+    _lib.check(_lib.lib().tilu_mg_prolong_add(coarse_level, cuda(e).data_ptr(), u.data_ptr(), st))
+    assert np.array_equal(u.cpu().numpy(), u0 + MO.prolong(e, coarse_level))
+
+
+@pytest.mark.parametrize("name", MG_CASES)
+def test_v_cycle_and_convergence_factor_vs_reference(name):
+    d = np.load(os.path.join(GOLDEN, name + ".npz"))
+    H = hierarchy(d, name)
+    top = H.top
+    f = cuda(d["f"])
+    u = H.zero(top)
+    # The reference multiplies by the assembled CSR matrix (different summation order from the stencil
+    # form, <= 1e-14 relative per product) and solves the coarsest level by PCG to 1e-12 |b|; the
+    # iterates agree to 1e-11 relative (lmin = 2: one coarse DoF, agreement ~1e-14).
+    tol = 1e-12 if int(d["lmin"]) == 2 else 1e-11
+    for k, ref in enumerate(d["u_cycles"]):
+        H.v_cycle(top, u, f)
+        err = float(np.abs(u.cpu().numpy() - ref).max() / np.abs(ref).max())
+        assert err <= tol, (name, k, err)
+    rho = H.convergence_factor(steps=int(d["rho_steps"]), seed=42)
+    assert abs(rho - float(d["rho"])) <= 1e-9 * float(d["rho"]), (rho, float(d["rho"]))
+
+
+def test_solve_reaches_tolerance():
+    H = MG.Hierarchy(lattice.unit_tet(), 2, 6, S.CoefficientField.constant(1.0),
+                     SmootherConfig(kind="surrogate_ilu", degrees=(3, 3, 3)), 2, 2)
+    g = lattice.grid_size(6)
+    f = cuda(np.where(lattice.interior_mask(6), np.random.default_rng(1).standard_normal(g), 0.0))
+    u, cycles = H.solve(f, tol=1e-10)
+    assert cycles <= 12
+    r = H.residual(H.top, u, f, H.zero(H.top))
+    assert float(torch.linalg.norm(r)) <= 1e-10 * float(torch.linalg.norm(f))
