@@ -170,6 +170,23 @@ int tilu_mg_restrict(int coarse_level, const double *r_fine, double *r_coarse, v
 int tilu_mg_prolong_add(int coarse_level, const double *e_coarse, double *u_fine, void *stream);
 int tilu_dense_mv(int m, const double *M, const double *x, double *y, void *stream);
 
+/* Interface stages of the hybrid multi-tet smoother (Hierarchy._interface_stage,
+ * multigrid.py:400-412).  DEVICE pointers unless stated.
+ * tilu_csr_residual_rows: r[i] = f[ids[i]] - sum_k data[k] u[indices[k]] over row i of a CSR row subset
+ *   (the rows `ids` of the global matrix, global column indices), in scipy's csr_matvec order.
+ * tilu_csr_tri_solve_blocks: nblocks independent CSR blocks stored back to back (rows roff[b]..roff[b+1]-1,
+ *   block-local int32 column indices): z = (lower | upper triangle incl. diagonal)^{-1} b per block
+ *   (_kernels.csr_lower_solve / csr_upper_solve, _kernels.py:490-519), then u[ids[row]] += z[row].  The
+ *   schedule (loff [nblocks+1] -> lptr [nlevels_total+1] -> perm, block-local rows grouped by dependency
+ *   level) comes from tilu_csr_levels (HOST pointers; returns the level count of one block, -1 on a bad
+ *   argument). */
+int tilu_csr_levels(int m, const int64_t *indptr, const int *indices, int upper, int *level);
+int tilu_csr_residual_rows(int64_t nrows, const int64_t *indptr, const int64_t *indices, const double *data,
+                           const int64_t *ids, const double *u, const double *f, double *r, void *stream);
+int tilu_csr_tri_solve_blocks(int nblocks, const int64_t *roff, const int64_t *indptr, const int *indices,
+                              const double *data, const int64_t *loff, const int64_t *lptr, const int *perm,
+                              int upper, const double *b, double *z, const int64_t *ids, double *u, void *stream);
+
 /* Host-side setup: rows [grid][15] (interior rows written, others untouched) of a separable scalar
  * coefficient on the unit macro-tet from its [3][4n+1] tables -- bitwise the reference's per-point
  * assembly stencil_source (assembly.py:208-221) for that coefficient.  HOST pointers. */

@@ -187,3 +187,24 @@ class Hierarchy:
                 raise RuntimeError("power iteration collapsed")
             e /= rho
         return rho
+
+
+class InnerSolveError(RuntimeError):
+    """The inner multigrid of a Schur interior solve stalled (reference schur.py:27-28)."""
+
+
+def schur_inner_solve(hier: Hierarchy, rhs: torch.Tensor, tol: float = 1e-8, max_cycles: int = 50) -> torch.Tensor:
+    """Interior solve A_tt^{-1} rhs of one macro-tet by V-cycles with the configured smoother -- the
+    'multigrid' branch of the reference's SchurComplement._inner_solve (schur.py:80-100): rhs holds the
+    interior DoF in lattice-rank order; returns the interior solution (CUDA tensors).  Raises
+    InnerSolveError when the residual stays above 10 tol |f| (schur.py:96-99)."""
+    lvl = hier.levels[hier.top]
+    idx = torch.as_tensor(lattice.lattice_rank(lattice.lattice_coords(lvl, "interior"), lvl), device=hier.device)
+    f = hier.zero(hier.top)
+    f.index_copy_(0, idx, rhs.to(hier.device, torch.float64))
+    u, _ = hier.solve(f, tol=tol, max_cycles=max_cycles)
+    r = hier.residual(hier.top, u, f, hier.zero(hier.top)) if hier.top > 0 else torch.zeros_like(f)
+    resid, nf = float(torch.linalg.norm(r)), float(torch.linalg.norm(f))
+    if resid > 10 * tol * nf:
+        raise InnerSolveError(f"inner multigrid stalled (residual {resid:.2e})")
+    return u.index_select(0, idx)

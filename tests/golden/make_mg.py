@@ -64,7 +64,24 @@ def case(name, tet, coeff, lmin, lmax, cfg, nu, cycles=3, steps=8):
     print(name, "rho", rho, "|u|", [float(np.abs(v).max()) for v in us])
 
 
+def schur_case():
+    """SchurComplement._inner_solve (schur.py:80-100, 'multigrid' inner solver) on cell 0 of the cube mesh."""
+    from tetilu.schur import SchurComplement
+    mesh = geometry.cube_mesh()
+    level = 4
+    sc = SchurComplement(mesh, level, inner="multigrid")
+    n_int = len(sc._cells[0]["ids"])
+    rhs = np.random.default_rng(3).standard_normal(n_int)
+    x = sc._inner_solve(0, rhs)
+    np.savez_compressed(os.path.join(OUT, "schur_inner_L4.npz"), level=level, rhs=rhs, x=x,
+                        verts=mesh.cell_tet(0).vertices, inner_tol=sc.inner_tol,
+                        degrees=np.array(sc.inner_smoother.degrees), kind=sc.inner_smoother.kind,
+                        variant=sc.inner_smoother.variant)
+    print("schur inner", n_int, float(np.abs(x).max()))
+
+
 if __name__ == "__main__":
+    schur_case()
     case("mg_unit_L5_surr", UNIT, CoefficientField.constant(1.0), 2, 5,
          SmootherConfig(kind="surrogate_ilu", degrees=(3, 3, 3), variant="v1"), 2)
     case("mg_unit_L5_ilu", UNIT, CoefficientField.constant(1.0), 2, 5, SmootherConfig(kind="ilu"), 1)
