@@ -608,6 +608,51 @@ def run_config3(args) -> dict:
     return out
 
 
+def run_widen() -> dict:
+    """The SURVEY 8(f) rows measured beside the hot path (a few seconds): on-device factorization vs the host
+    routine at config 4's / config 5's levels, and the multigrid V-cycle around the smoother (level 7)."""
+    import torch
+
+    from paper_2210_15280_b200 import SmootherConfig, _lib, fitting, lattice, multigrid, stencil
+
+    out = {"factorize": [], "multigrid": None}
+    for level in (7, 8):
+        src = stencil.stencil_source(lattice.unit_tet(), level, stencil.CoefficientField.constant(1.0))
+        band = lattice.band_ranks(level)
+        fitting.factorize_tet_device(src, level, full_store=False, collect_ranks=band)
+        _lib.profile_enable(True)
+        dev = fitting.factorize_tet_device(src, level, full_store=False, collect_ranks=band)
+        torch.cuda.synchronize()
+        prof = _lib.profile_read()
+        _lib.profile_enable(False)
+        t = time.perf_counter()
+        host = fitting.factorize_tet(src, level, full_store=False, collect_ranks=band)
+        th = time.perf_counter() - t
+        kms = prof["factorize"][1] / prof["factorize"][0]
+        n_int = interior_count(level)
+        out["factorize"].append({"level": level, "kernel_ms": kms, "host_ms": th * 1e3, "points_per_s": n_int / (kms * 1e-3),
+                                 "algorithmic_gbs": n_int * 72 / (kms * 1e-3) / 1e9, "wavefronts": 3 * 2 ** level - 11,
+                                 "bitwise_equal_host": bool(np.array_equal(dev.collected, host.collected))})
+    lmax = 7
+    H = multigrid.Hierarchy(lattice.unit_tet(), 2, lmax, stencil.CoefficientField.constant(1.0),
+                            SmootherConfig(kind="surrogate_ilu", degrees=(3, 3, 3)), 2, 2, factorize="device")
+    rho = H.convergence_factor(steps=8)
+    g = lattice.grid_size(lmax)
+    f = torch.as_tensor(np.where(interior_mask(lmax), np.random.default_rng(1).standard_normal(g), 0.0), device="cuda")
+    u = H.zero(H.top)
+    H.v_cycle(H.top, u, f)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(5):
+        H.v_cycle(H.top, u, f)
+    b.record()
+    torch.cuda.synchronize()
+    out["multigrid"] = {"lmin": 2, "lmax": lmax, "nu_pre": 2, "nu_post": 2, "smoother": "surrogate_ilu (3,3,3) V1",
+                        "convergence_factor": rho, "ms_per_v_cycle": a.elapsed_time(b) / 5, "dofs": interior_count(lmax)}
+    return out
+
+
 def run_ours(args, D: Dist):
     import torch
 
@@ -741,6 +786,13 @@ def run_ours(args, D: Dist):
             traceback.print_exc()
             c3 = {"error": f"{type(e).__name__}: {e}"}
 
+    widen = None
+    if D.world == 1 and D.rank == 0 and not args.no_widen:
+        try:
+            widen = run_widen()
+        except Exception as e:
+            widen = {"error": f"{type(e).__name__}: {e}"}
+
     if D.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D.world, "steps": args.steps,
@@ -758,7 +810,7 @@ def run_ours(args, D: Dist):
             "cpu_baseline": cpu, "cpu_baseline_port": cpu_port, "e2e": e2e, "e2e_multi": e2e_multi,
             "gpu_launches": launches, "kernels": kernels, "clocks": clk, "distributed": D.info(),
             "residual_norm2_last": float(norms[-1][-1]) if norms else None,
-            "config3": c3,
+            "config3": c3, "widen": widen,
         }
         print(json.dumps(line), flush=True)
 
@@ -775,6 +827,7 @@ def main():
     ap.add_argument("--simple", action="store_true", help="force the reference-layout kernels")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline legs")
     ap.add_argument("--no-single", action="store_true", help="skip the config-3 (level 9 single tet) leg")
+    ap.add_argument("--no-widen", action="store_true", help="skip the SURVEY 8(f) leg (factorization, multigrid)")
     ap.add_argument("--config3-sweeps", type=int, default=CFG3["sweeps"])
     args = ap.parse_args()
     if args.warmup < 3:

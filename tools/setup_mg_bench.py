@@ -33,8 +33,20 @@ def time_factor(level, kind, reps=3):
         dev = F.factorize_tet_device(src, level, full_store=False, collect_ranks=band)
         torch.cuda.synchronize()
         td.append(time.perf_counter() - t)
-    out = {"level": level, "rows": kind, "interior": lattice.interior_size(level),
-           "device_s": min(td), "device_points_per_s": lattice.interior_size(level) / min(td)}
+    from paper_2210_15280_b200 import _lib
+    _lib.profile_enable(True)
+    F.factorize_tet_device(src, level, full_store=False, collect_ranks=band)
+    torch.cuda.synchronize()
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    kms = prof["factorize"][1] / prof["factorize"][0]
+    n_int = lattice.interior_size(level)
+    out = {"level": level, "rows": kind, "interior": n_int, "wavefronts": 3 * 2 ** level - 11,
+           "device_s": min(td), "device_points_per_s": n_int / min(td),
+           "kernel_ms": kms, "kernel_us_per_wavefront": 1e3 * kms / (3 * 2 ** level - 11),
+           # algorithmic bytes: the 72-byte factor row written per point (+ 120 B of per-point operator rows when
+           # they are read; constant / on-the-fly rows read nothing)
+           "kernel_algorithmic_gbs": n_int * 72 / (kms * 1e-3) / 1e9}
     if kind == "const" or level <= 8:
         hsrc = src if kind == "const" else S.stencil_source(lattice.unit_tet(), level, S.sin_kappa())
         t = time.perf_counter()
