@@ -489,6 +489,15 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
     P.arow = dsepk ? nullptr : darow;
     P.arows = (dsepk || d->arow) ? nullptr : d->arows_dev;
     P.factors = dfactors ? dfactors : d->factors_dev;
+    {
+        const double zeros[15] = {};
+        double *dz = nullptr;
+        if ((rc = dev_upload(p, &dz, zeros, 15))) {
+            tilu_plan_destroy(p);
+            return rc;
+        }
+        p->zrow = dz;
+    }
     if (d->acoefs) {
         P.akx1 = d->akx1;
         p->ky1a = d->aky1;
@@ -526,12 +535,60 @@ int tilu_plan_create(const tilu_desc_t *d, tilu_plan_t **out)
     return TILU_OK;
 }
 
+static int sweep_common(const tilu_plan_t *p, double *u, const double *f, int ntets, int sweeps, double *rnorm2,
+                        bool stored, void *stream);
+
+// solve_into on the fast kernels: w <- (L D L^T)^{-1} w is one smoothing step from u = 0 with right-hand side
+// w and a ZERO operator row -- the residual f - 0 u is f bit for bit, and u = 0 + w' is w' -- so the plane /
+// batched sweep kernels serve the drop-in method at their speed (the one-CTA-per-tet reference-layout kernels
+// are ~10x slower from level 6 up).  The plan copy only swaps the operator; lazily built members (plane
+// workspace, coefficient tables) created during the call are handed back to the plan.
+static int solve_via_sweep(const tilu_plan_t *p, double *w, int ntets, bool stored, cudaStream_t s)
+{
+    static std::mutex mu;  // two first calls on one plan must not both create its workspace
+    std::unique_lock<std::mutex> lk(mu, std::defer_lock);
+    if ((ntets == 1 && !p->plane) || (ntets > 1 && !p->coef)) lk.lock();
+    tilu_plan q = *p;
+    q.dev.arow = p->zrow;
+    q.dev.arows = nullptr;
+    q.dev.sepk = nullptr;
+    q.dev.seedA = nullptr;
+    std::memset(q.harow, 0, sizeof(q.harow));
+    Scratch sc(s);
+    const size_t nd = (size_t)ntets * p->dev.grid;
+    double *u0 = sc.get(nd);
+    if (!u0) return fail(TILU_ENOMEM, "scratch allocation failed");
+    cudaMemsetAsync(u0, 0, nd * sizeof(double), s);
+    const int rc = sweep_common(&q, u0, w, ntets, 1, nullptr, stored, s);
+    tilu_plan *mp = const_cast<tilu_plan *>(p);
+    if (!mp->plane && q.plane) mp->plane = q.plane;
+    if (!mp->coef && q.coef) mp->coef = q.coef;
+    if (rc) return rc;
+    const int nl = g_launches;
+    cudaMemcpyAsync(w, u0, nd * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    g_launches = nl;
+    return check_cuda("solve (sweep route)");
+}
+
+static bool sweep_route_fast(const tilu_plan_t *p, int ntets, bool stored)
+{
+    if (p->flags & TILU_SCHED_SIMPLE) return false;
+    tilu_plan q = *p;
+    q.dev.arow = p->zrow;
+    q.dev.seedA = nullptr;
+    const bool plane = ntets == 1 && plane_supported(&q) && !(p->flags & TILU_SCHED_BATCH) &&
+                       ((p->flags & TILU_SCHED_PLANE) || p->dev.level >= plane_min_level());
+    const bool batch = !stored && batch_ok(&q) && (ntets >= 2 || p->dev.level >= 6);
+    return plane || batch;
+}
+
 static int solve_common(const tilu_plan_t *p, double *w, int ntets, int which, bool stored, void *stream)
 {
     g_launches = 0;
     if (!valid_plan(p) || !w || ntets < 1) return fail(TILU_EINVAL, "invalid plan / vector / ntets");
     if (stored && !p->dev.factors) return fail(TILU_EINVAL, "plan has no stored factors");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (which == 3 && p->zrow && sweep_route_fast(p, ntets, stored)) return solve_via_sweep(p, w, ntets, stored, s);
     Scratch sc(s);
     double *state = nullptr;
     if (!stored && !(state = sc.get((size_t)ntets * p->dev.nrows * 8 * p->dev.kx1)))

@@ -37,6 +37,9 @@
 
 namespace tilu {
 
+#ifndef TILU_BWD_MINB2
+#define TILU_BWD_MINB2 3   // resident CTAs per SM the backward kernel (2 tets per lane) is compiled for
+#endif
 constexpr int kWarps = 4;  // warps per CTA (independent; the CTA is only an occupancy unit)
 constexpr long long kSent = 0x7FF4DEADBEEF0001ll;  // signalling NaN: "not yet computed"
 
@@ -337,11 +340,21 @@ __device__ __forceinline__ void fwd_band_load(double &dst, const PlanDev &P, con
 }
 
 // Shared memory of the forward / backward kernels: per warp, D mbarriers + D ring stages.
-constexpr int kChunk = 2;   // points per ring stage (per bulk copy)
+constexpr int kChunk = 2;   // points per ring stage (per bulk copy), backward
 template <int T>
-constexpr int kStages = 2;  // ring depth in chunks (kStages * kChunk points in flight per warp)
-template <int NS, int T, int D>
-constexpr size_t ring_smem() { return (size_t)kWarps * D * (8 + (NS * kChunk * 32 * T + 8 * kChunk) * 8); }
+constexpr int kStages = 2;  // ring depth in chunks (kStages * kChunk points in flight per warp), backward
+#ifndef TILU_FWD_CHUNK
+#define TILU_FWD_CHUNK 2
+#endif
+#ifndef TILU_FWD_STAGES
+#define TILU_FWD_STAGES 2
+#endif
+#ifndef TILU_FWD_MINB2
+#define TILU_FWD_MINB2 3   // resident CTAs per SM the forward kernel (2 tets per lane) is compiled for
+#endif
+constexpr int kChunkF = TILU_FWD_CHUNK, kStagesF = TILU_FWD_STAGES;  // the same for the forward ring
+template <int NS, int T, int D, int PC = kChunk>
+constexpr size_t ring_smem() { return (size_t)kWarps * D * (8 + (NS * PC * 32 * T + 8 * PC) * 8); }
 constexpr int kFwdNS = 8;    // forward ring streams: ue us un ubn ubc uts utc f
 constexpr int kBwdNS = 2;    // backward ring streams: w_f(p), u(p)
 
@@ -377,9 +390,9 @@ __device__ __forceinline__ void smem_march_rt(double *tab, int M, int K, int lan
 
 // AMODE: 0 = per-point rows, 1 = constant row, 3 = operator surrogate (marched weights).
 template <int K, bool EXACT, int AMODE, int T, bool TAB>
-__global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_batch_fwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? TILU_FWD_MINB2 : 2)) k_batch_fwd(PlanDev P, BatchArgs A)
 {
-    constexpr int GW = 32 * T, D = kStages<T>, NS = kFwdNS, PC = kChunk;
+    constexpr int GW = 32 * T, D = kStagesF, NS = kFwdNS, PC = kChunkF;
     using RingT = Ring<NS, GW, D, PC>;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_tab[kWarps][7 * K];
@@ -676,7 +689,7 @@ __device__ __forceinline__ int bwd_band_load(double &dst, const BwdRow &R, const
 }
 
 template <int K, bool EXACT, int T, bool TAB>
-__global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? 3 : 2)) k_batch_bwd(PlanDev P, BatchArgs A)
+__global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? TILU_BWD_MINB2 : 2)) k_batch_bwd(PlanDev P, BatchArgs A)
 {
     constexpr int GW = 32 * T, D = kStages<T>, NS = kBwdNS, PC = kChunk;
     using RingT = Ring<NS, GW, D, PC>;
@@ -1099,7 +1112,7 @@ static unsigned persistent_grid(Kern k, size_t smem)
 template <int K, int T, bool TAB>
 static void launch_fwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_t s)
 {
-    constexpr size_t sm = ring_smem<kFwdNS, T, kStages<T>>();
+    constexpr size_t sm = ring_smem<kFwdNS, T, kStagesF, kChunkF>();
     auto run = [&](auto kern) { launch_persistent<decltype(kern)>(kern, sm, P, A, s); };
     const int am = P.seedA ? 3 : P.arow ? 1 : 0;
     if (exact) {

@@ -58,6 +58,7 @@ struct tilu_plan {
     void *coef;  // coefficient tables (2 x [grid][8] doubles), lazily built; freed with the plan
     void *plane;  // plane-layout workspace of the single-tet path (tilu_plane.cu), lazily built
     // owned device allocations
-    void *allocs[16];
+    const double *zrow;  // DEVICE [15] zeros: the operator row of solve_into routed through a sweep (r = f exactly)
+    void *allocs[20];
     int nallocs;
 };

@@ -101,3 +101,34 @@ def test_operator_surrogate_batched_kernels(level, ntets, fast):
         else:
             assert np.array_equal(got[t], ref)
         np.testing.assert_allclose(rn.cpu().numpy()[:, t], nr, rtol=1e-10 if fast else 1e-12)
+
+
+@pytest.mark.parametrize("level,ntets,stored", [(5, 1, False), (6, 1, False), (7, 1, False), (5, 3, False), (6, 40, False),
+                                                (6, 1, True)])
+def test_solve_into_fast_route_equals_reference_layout_kernels(level, ntets, stored):
+    """The drop-in solve_into runs on the plane / batched sweep kernels (one step from u = 0 with a zero
+    operator row: r = f exactly); it must equal the reference-layout wavefront kernels bit for bit, with or
+    without an operator on the plan."""
+    src = S.stencil_source(lattice.distorted_tet(), level, S.diag_tensor((1, 1e-2, 1)))
+    mask = lattice.interior_mask(level)
+    w0 = np.zeros((ntets, lattice.grid_size(level)))
+    w0[:, mask] = np.random.default_rng(level).standard_normal((ntets, int(mask.sum())))
+    outs = []
+    if stored:
+        fac = F.factorize_tet(src, level).rows
+        z = np.zeros((7, 1, 1, 1))
+        for sched in ("auto", "simple"):
+            p = DevicePlan(level, z, np.zeros(1), "v2", factors=fac, schedule=sched)
+            w = cuda(w0[0])
+            p.stored_solve_into(w)
+            outs.append(w.cpu().numpy())
+    else:
+        fit = F.fit_surrogate_ilu(src, level, (3, 3, 3), "v1")
+        for sched, op in (("auto", {}), ("auto", {"arows": src.data}), ("simple", {})):
+            p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, schedule=sched, **op)
+            w = cuda(w0 if ntets > 1 else w0[0])
+            p.solve_into(w)
+            outs.append(w.cpu().numpy())
+    for o in outs[:-1]:
+        assert np.array_equal(o, outs[-1])
+    assert not np.any(outs[0].reshape(ntets, -1)[:, ~mask])
