@@ -594,6 +594,20 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                 sepk_window(P.sepk + T4, live ? 4 * y : 4, gyw);
                 sepk_window(P.sepk + 2 * T4, live ? 4 * z : 4, gzw);
             }
+            // operator surrogate (AMODE 3, a_mode='surrogate'): the 15 weights of a point are the heads of 15
+            // forward-difference tables seeded per row (P.seedA, runtime extent akx1 <= AKMAX, zero-padded: the
+            // padding entries add 0.0 and never reach an entry that is read) and marched after every point
+            // (_kernels.py:444-483 surrogate_apply_residual)
+            constexpr int AKMAX = 4;
+            double da[AMODE == 3 ? 15 : 1][AMODE == 3 ? AKMAX : 1];
+            if (AMODE == 3) {
+                const int ak = P.akx1;
+                const double *sd = P.seedA + (int64_t)(live ? row_id(n, z, y) : 0) * 15 * ak;
+#pragma unroll
+                for (int m = 0; m < 15; ++m)
+#pragma unroll
+                    for (int j = 0; j < AKMAX; ++j) da[m][j] = (live && j < ak) ? sd[m * ak + j] : 0.0;
+            }
             auto issue = [&](int q) {  // lane 0: u box (planes s-1..s+1, lines tq-2 .. tq+GS+1) + f box
                 const int sl = tiss % NT;
                 const int tq = T0 + GS * q;
@@ -634,7 +648,10 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                     if (false) {  // experiment: residual helper without arithmetic (results invalid)
 #endif
                         double a[15];
-                        if (AMODE == 2) {
+                        if (AMODE == 3) {
+#pragma unroll
+                            for (int qq = 0; qq < 15; ++qq) a[qq] = da[qq][0];
+                        } else if (AMODE == 2) {
                             double hxw[7];
                             sepk_window(P.sepk, 4 * (sg - z), hxw);
                             sepk_row(hxw, gyw, gzw, P.sepk_c0, P.sepk_w, a);
@@ -647,6 +664,29 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
 #pragma unroll
                             for (int qq = 0; qq < 15; ++qq) a[qq] = ar[qq];
                         }
+                        if (AMODE == 3) {
+                            // surrogate_apply_residual order (_kernels.py:470-480): every product subtracted
+                            // from the running value f - c u - w .. - tw
+                            double rr = msub<EXACT>(tb[FOFF], a[7], u1[2 * Wn]);
+                            rr = msub<EXACT>(rr, a[0], u1[1 * Wn]);
+                            rr = msub<EXACT>(rr, a[1], u0[2 * Wn]);
+                            rr = msub<EXACT>(rr, a[2], u0[3 * Wn]);
+                            rr = msub<EXACT>(rr, a[3], u1[0 * Wn - 1]);
+                            rr = msub<EXACT>(rr, a[4], u1[1 * Wn - 1]);
+                            rr = msub<EXACT>(rr, a[5], u0[1 * Wn - 1]);
+                            rr = msub<EXACT>(rr, a[6], u0[2 * Wn - 1]);
+                            rr = msub<EXACT>(rr, a[8], u1[3 * Wn]);
+                            rr = msub<EXACT>(rr, a[9], u2[2 * Wn]);
+                            rr = msub<EXACT>(rr, a[10], u2[1 * Wn]);
+                            rr = msub<EXACT>(rr, a[11], u1[4 * Wn + 1]);
+                            rr = msub<EXACT>(rr, a[12], u1[3 * Wn + 1]);
+                            rr = msub<EXACT>(rr, a[13], u2[3 * Wn + 1]);
+                            rr = msub<EXACT>(rr, a[14], u2[2 * Wn + 1]);
+                            res = rr;
+                            r2 = fma(res, res, r2);
+#pragma unroll
+                            for (int qq = 0; qq < 15; ++qq) march<AKMAX>(da[qq]);
+                        } else {
                         // stencil_apply order (_kernels.py:243-267): c, w s se bnw bn bc be, e n nw tse ts tc tw
                         double out = EXACT ? dmul(a[7], u1[2 * Wn]) : a[7] * u1[2 * Wn];
                         out = madd<EXACT>(out, a[0], u1[1 * Wn]);        // w   (s,   sg-1, z)
@@ -665,6 +705,7 @@ __global__ void __launch_bounds__(3 * PW * 32, 1) k_plane_fwd(const PlanDev P, c
                         out = madd<EXACT>(out, a[14], u2[2 * Wn + 1]);   // tw  (s+1, sg,   z+1)
                         res = dsub(tb[FOFF], out);
                         r2 = fma(res, res, r2);
+                        }
                     }
                     rg[j * (32 * RS) + 7] = res;
                 }
@@ -1154,7 +1195,8 @@ static bool launch_e(const PlanDev &P, const Args &A, const Maps &M, int ctas, b
 }
 static bool launch_pass(const PlanDev &P, const Args &A, const Maps &M, int ctas, bool exact, bool fwd, cudaStream_t s)
 {
-    const int am = P.sepk ? 2 : P.arow ? 1 : 0;
+    const int am = P.seedA ? 3 : P.sepk ? 2 : P.arow ? 1 : 0;
+    if (am == 3) return exact ? launch_e<true, 3>(P, A, M, ctas, fwd, s) : launch_e<false, 3>(P, A, M, ctas, fwd, s);
     if (exact) return am == 2 ? launch_e<true, 2>(P, A, M, ctas, fwd, s)
                     : am == 1 ? launch_e<true, 1>(P, A, M, ctas, fwd, s) : launch_e<true, 0>(P, A, M, ctas, fwd, s);
     return am == 2 ? launch_e<false, 2>(P, A, M, ctas, fwd, s)
@@ -1291,7 +1333,9 @@ bool plane_supported(const tilu_plan *p)
     if (p->flags & TILU_SCHED_SIMPLE) return false;
     static const char *e = std::getenv("TILU_PLANE");
     if (e && e[0] == '0') return false;
-    return p->dev.kx1 <= 6 && p->dev.level >= 3 && p->dev.level <= 10 && p->dev.seedA == nullptr &&
+    // operator surrogate (seedA): x extent up to 4 (a_degrees <= 3) in the residual helper's registers
+    if (p->dev.seedA != nullptr) return p->dev.kx1 <= 6 && p->dev.level >= 3 && p->dev.level <= 10 && p->dev.akx1 <= 4;
+    return p->dev.kx1 <= 6 && p->dev.level >= 3 && p->dev.level <= 10 &&
            (p->dev.arow != nullptr || p->dev.arows != nullptr || p->dev.sepk != nullptr);
 }
 

@@ -132,3 +132,29 @@ def test_solve_into_fast_route_equals_reference_layout_kernels(level, ntets, sto
     for o in outs[:-1]:
         assert np.array_equal(o, outs[-1])
     assert not np.any(outs[0].reshape(ntets, -1)[:, ~mask])
+
+
+@pytest.mark.parametrize("level,adeg,fast", [(5, (3, 3, 3), False), (7, (2, 2, 2), False), (7, (3, 3, 3), False),
+                                             (6, (1, 1, 1), False), (6, (3, 3, 3), True)])
+def test_operator_surrogate_in_plane_kernels(level, adeg, fast):
+    """a_mode='surrogate' on one macro-tet from level 5 up runs in the plane kernels' residual helper
+    (15 marched tables in registers); bitwise vs the oracle's surrogate_apply_residual sweep, the fast (FMA)
+    mode within 1e-12."""
+    src = S.stencil_source(lattice.unit_tet(), level, S.sin_kappa())
+    fit = F.fit_surrogate_ilu(src, level, (4, 4, 4), "v1")
+    ac = F.fit_surrogate_operator(src, level, adeg)
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, acoefs=ac, fast=fast)
+    u0 = u0_of(level)[0]
+    f = np.zeros_like(u0)
+    f[lattice.interior_mask(level)] = np.random.default_rng(2).standard_normal(lattice.interior_size(level))
+    u = cuda(u0)
+    rn = p.sweep(u, cuda(f), 3, norms=True)
+    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows)
+    ref = u0.copy()
+    O.sweeps(sur, level, None, ref, f, 3, acoefs=ac)
+    got = u.cpu().numpy()
+    if fast:
+        assert float(np.abs(got - ref).max() / np.abs(ref).max()) <= 1e-12
+    else:
+        assert np.array_equal(got, ref)
+    assert rn.shape == (3, 1) and np.all(np.isfinite(rn.cpu().numpy()))

@@ -190,3 +190,12 @@ def test_schur_inner_solve_vs_reference():
     # both stop at the first cycle whose residual is below 1e-8 |f|: the same cycle, so the iterates agree
     # to rounding (1e-11 relative); two different cycle counts would still agree to ~1e-8
     assert float(np.abs(x.cpu().numpy() - ref).max() / np.abs(ref).max()) <= 1e-11
+
+
+def test_convergence_factor_level6_vs_reference():
+    d = np.load(os.path.join(GOLDEN, "mgrho_unit_L6.npz"))
+    cfg = SmootherConfig(kind=str(d["kind"]), degrees=tuple(int(v) for v in d["degrees"]), variant=str(d["variant"]))
+    H = MG.Hierarchy(d["verts"], int(d["lmin"]), int(d["lmax"]), S.CoefficientField.constant(1.0), cfg,
+                     int(d["nu"]), int(d["nu"]), factorize="device")
+    rho = H.convergence_factor(steps=int(d["rho_steps"]), seed=42)
+    assert abs(rho - float(d["rho"])) <= 1e-9 * float(d["rho"]), (rho, float(d["rho"]))
