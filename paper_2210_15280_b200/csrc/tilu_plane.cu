@@ -1058,6 +1058,25 @@ __global__ void __launch_bounds__(256) k_plane_xpose(const PlanDev P, Geo g, con
         }
     }
 }
+// Boundary values of u (x = 0, y = 0, z = 0 or x + y + z = n) into the plane layout: the residual reads them
+// as given (the all-Dirichlet case has zeros there; the cell stage of a hybrid mesh carries the shared
+// interface values, multigrid.py:414-429).  The kernels never write these positions; copied on every call
+// because the planes persist between calls.  grid = (y, z) over the closed lattice, threads over x.
+__global__ void __launch_bounds__(128) k_plane_pack_boundary(int n, Geo g, const double *__restrict__ src,
+                                                             double *__restrict__ dst)
+{
+    const int y = blockIdx.x, z = blockIdx.y;
+    if (y + z > n) return;
+    const int xm = n - y - z;
+    const int64_t base = row_offset(n, z, y);
+    if (y == 0 || z == 0) {
+        for (int x = threadIdx.x; x <= xm; x += blockDim.x) dst[pidx(g, y + z, x + z, z)] = src[base + x];
+    } else if (threadIdx.x < 2) {
+        const int x = threadIdx.x ? xm : 0;
+        dst[pidx(g, y + z, x + z, z)] = src[base + x];
+    }
+}
+
 static void launch_xpose(const PlanDev &P, const Geo &g, const double *src, double *dst, bool unpack, cudaStream_t s)
 {
     const int n = P.n;
@@ -1395,6 +1414,8 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
     }
     prof_begin(s);
     launch_xpose(P, w->g, u, w->u, false, s);
+    k_plane_pack_boundary<<<dim3(P.n + 1, P.n + 1), 128, 0, s>>>(P.n, w->g, u, w->u);
+    ++nl;
     launch_xpose(P, w->g, f, w->f, false, s);
     if (!w->armed) {
         k_plane_arm<<<P.nrows, 128, 0, s>>>(P, w->g, w->W);

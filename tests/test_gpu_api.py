@@ -158,3 +158,33 @@ def test_operator_surrogate_in_plane_kernels(level, adeg, fast):
     else:
         assert np.array_equal(got, ref)
     assert rn.shape == (3, 1) and np.all(np.isfinite(rn.cpu().numpy()))
+
+
+@pytest.mark.parametrize("level", [4, 5, 6])
+@pytest.mark.parametrize("sched", ["simple", "plane", "batch", "auto"])
+@pytest.mark.parametrize("ntets", [1, 3])
+def test_boundary_values_are_read_as_given(level, sched, ntets):
+    """The cell stage of a hybrid mesh hands tets whose boundary entries carry the shared interface values
+    (multigrid.py:414-429): every kernel family reads them in the residual and never writes them."""
+    src = S.stencil_source(lattice.distorted_tet(), level, S.diag_tensor((1, 1, 1e-1)))
+    fit = F.fit_surrogate_ilu(src, level, (3, 3, 3), "v1")
+    g = lattice.grid_size(level)
+    mask = lattice.interior_mask(level)
+    rng = np.random.default_rng(level)
+    u0 = rng.uniform(-1, 1, g)
+    f = np.where(mask, rng.standard_normal(g), 0.0)
+    ref = u0.copy()
+    O.sweeps(O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows), level, src.data, ref, f, 2)
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arows=src.data, schedule=sched)
+    u = cuda(np.tile(u0, (ntets, 1)) if ntets > 1 else u0)
+    p.sweep(u, cuda(np.tile(f, (ntets, 1)) if ntets > 1 else f), 2)
+    got = u.cpu().numpy().reshape(ntets, -1)
+    for t in range(ntets):
+        assert np.array_equal(got[t], ref)
+    # a later all-Dirichlet call on the same plan must not see the old boundary values (the planes persist)
+    z0 = np.where(mask, u0, 0.0)
+    ref0 = z0.copy()
+    O.sweeps(O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows), level, src.data, ref0, f, 1)
+    u = cuda(z0)
+    p.sweep(u, cuda(f), 1)
+    assert np.array_equal(u.cpu().numpy(), ref0)
