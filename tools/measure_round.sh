@@ -13,7 +13,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 LEVEL=9 SWEEPS=4 COEF=sin timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_plane_(fwd|bwd)" \
     -s 4 -c 2 -o $O/${T}_plane_full -f python tools/plane_bench.py > $O/${T}_plane_ncu.log 2>&1
 ncu -i $O/${T}_plane_full.ncu-rep --page raw --csv > $O/${T}_plane_full_raw.csv 2>/dev/null
+rm -f $O/${T}_plane_full.ncu-rep   # gpurun copies back at most 64 MiB: keep the exported pages only
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_batch_(fwd|bwd)" -s 2 -c 2 \
     -o $O/${T}_batch_full -f python tools/prof_batch.py --sweeps 3 > $O/${T}_batch_ncu.log 2>&1
 ncu -i $O/${T}_batch_full.ncu-rep --page raw --csv > $O/${T}_batch_full_raw.csv 2>/dev/null
+rm -f $O/${T}_batch_full.ncu-rep
 echo done
