@@ -67,3 +67,62 @@ def test_config2_full_distorted_level7_bitwise():
     ref = u0.copy()
     O.sweeps(_surrogate(sm), level, src.data, ref, f, sweeps)
     assert np.array_equal(u.cpu().numpy(), ref)
+
+
+def test_solve_into_level8_vs_oracle_bitwise():
+    """The drop-in SurrogateILU.solve_into at config 5's size (level 8, 2.7M DoF) runs on the plane kernels
+    (zero-operator sweep route) and equals the oracle's surrogate_forward + surrogate_backward bit for bit."""
+    from paper_2210_15280_b200 import build_surrogate_ilu
+    level = 8
+    src = stencil.stencil_source(lattice.unit_tet(), level, stencil.CoefficientField.constant(1.0))
+    pre = build_surrogate_ilu(src, level, (4, 4, 4), "v1", factorize="device")
+    mask = lattice.interior_mask(level)
+    w0 = np.zeros(mask.size)
+    w0[mask] = np.random.default_rng(8).standard_normal(int(mask.sum()))
+    w = torch.as_tensor(w0, device="cuda")
+    pre.solve_into(w)
+    ref = w0.copy()
+    O.OracleSurrogate(level, pre.lcoefs, pre.dcoefs, pre.variant, pre.band_ranks, pre.store_rows).solve_into(ref)
+    assert np.array_equal(w.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("level,kind", [(8, "const"), (8, "sepk"), (9, "const")])
+def test_device_factorization_full_size_bitwise(level, kind):
+    """On-device factorization at config 5's / config 3's level against the host routine: the band rows and
+    a strided sample of the interior rows (the arrays the fit consumes) bit for bit."""
+    from paper_2210_15280_b200 import fitting
+    coeff = stencil.CoefficientField.constant(1.0) if kind == "const" else stencil.sin_kappa()
+    src = stencil.stencil_source(lattice.unit_tet(), level, coeff)
+    inner = lattice.lattice_rank(lattice.lattice_coords(level, "interior")[::97], level)
+    ranks = np.unique(np.concatenate([lattice.band_ranks(level), inner]))
+    host = fitting.factorize_tet(src, level, full_store=False, collect_ranks=ranks)
+    dev = fitting.factorize_tet_device(src, level, full_store=False, collect_ranks=ranks)
+    assert np.array_equal(dev.collected, host.collected)
+
+
+def test_transfers_adjoint_and_v_cycle_level8():
+    """Multigrid at level 8 (2.7M DoF): <P^T r, e> = <r, P e> to rounding on the device, and V-cycles contract
+    the residual by the level-independent factor (rho < 0.1 per cycle for the (3,3,3) surrogate smoother)."""
+    from paper_2210_15280_b200 import multigrid as MG
+    H = MG.Hierarchy(lattice.unit_tet(), 2, 8, stencil.CoefficientField.constant(1.0),
+                     SmootherConfig(kind="surrogate_ilu", degrees=(3, 3, 3)), 2, 2, factorize="device")
+    top = H.top
+    g8, g7 = lattice.grid_size(8), lattice.grid_size(7)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    m8 = torch.as_tensor(lattice.interior_mask(8), device="cuda")
+    m7 = torch.as_tensor(lattice.interior_mask(7), device="cuda")
+    r = torch.where(m8, torch.randn(g8, dtype=torch.float64, device="cuda", generator=gen), 0.0)
+    e = torch.where(m7, torch.randn(g7, dtype=torch.float64, device="cuda", generator=gen), 0.0)
+    lhs = float(torch.dot(H.restrict(top, r), e))
+    pe = H.zero(top)
+    H.prolongate_add(top, e, pe)
+    rhs = float(torch.dot(r, pe))
+    assert abs(lhs - rhs) <= 1e-11 * max(abs(lhs), abs(rhs), 1.0)
+    f = r
+    u = H.zero(top)
+    res = [float(torch.linalg.norm(f))]
+    for _ in range(4):
+        H.v_cycle(top, u, f)
+        res.append(float(torch.linalg.norm(H.residual(top, u, f, H.zero(top)))))
+    ratios = [b / a for a, b in zip(res[:-1], res[1:])]
+    assert all(q < 0.15 for q in ratios), ratios
