@@ -179,7 +179,11 @@ int tilu_dense_mv(int m, const double *M, const double *x, double *y, void *stre
  *   (_kernels.csr_lower_solve / csr_upper_solve, _kernels.py:490-519), then u[ids[row]] += z[row].  The
  *   schedule (loff [nblocks+1] -> lptr [nlevels_total+1] -> perm, block-local rows grouped by dependency
  *   level) comes from tilu_csr_levels (HOST pointers; returns the level count of one block, -1 on a bad
- *   argument). */
+ *   argument).
+ * tilu_csr_matvec: y = M x or y += M x (accumulate) for a CSR matrix in scipy's csr_matvec order -- the
+ *   transfers P e and P^T r (P^T passed as CSR) of a macro-mesh hierarchy (multigrid.py:377-388). */
+int tilu_csr_matvec(int64_t nrows, const int64_t *indptr, const int64_t *indices, const double *data,
+                    const double *x, double *y, int accumulate, void *stream);
 int tilu_csr_levels(int m, const int64_t *indptr, const int *indices, int upper, int *level);
 int tilu_csr_residual_rows(int64_t nrows, const int64_t *indptr, const int64_t *indices, const double *data,
                            const int64_t *ids, const double *u, const double *f, double *r, void *stream);

@@ -14,7 +14,7 @@ Public names mirror the reference's (tetilu/__init__.py:4-18) where they exist.
 from .fitting import (EmptySampleSet, FactorizationResult, PivotBreakdown, RankDeficientFit,
                       SurrogatePolynomial, factorize_tet, factorize_tet_device, lsq_fit, nddf_row_evaluate,
                       sample_coords)
-from .hybrid import HybridSmoother, InterfaceStage
+from .hybrid import HybridHierarchy, HybridSmoother, InterfaceStage
 from .lattice import grid_size, interior_size, kuhn_mesh, rank_tables
 from .multigrid import Hierarchy, InnerSolveError, schur_inner_solve
 from .partition import MacroMeshSmoother, allreduce_norms, partition
@@ -28,5 +28,5 @@ __all__ = [
     "sample_coords", "SurrogatePolynomial", "FactorizationResult", "RankDeficientFit",
     "EmptySampleSet", "PivotBreakdown", "SurrogateILUSmoother", "MacroMeshSmoother", "DevicePlan",
     "partition", "allreduce_norms", "grid_size", "interior_size", "rank_tables", "kuhn_mesh",
-    "factorize_tet_device", "Hierarchy", "schur_inner_solve", "InnerSolveError", "HybridSmoother", "InterfaceStage",
+    "factorize_tet_device", "Hierarchy", "schur_inner_solve", "InnerSolveError", "HybridSmoother", "HybridHierarchy", "InterfaceStage",
 ]

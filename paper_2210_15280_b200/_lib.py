@@ -50,7 +50,7 @@ EXPORTS = (
     "tilu_packed_scratch_size", "tilu_pack",
     "tilu_unpack", "tilu_sweep_packed", "tilu_plane_tasks", "tilu_sepk_rows",
     "tilu_factorize_device", "tilu_gather_rows", "tilu_mg_restrict", "tilu_mg_prolong_add", "tilu_dense_mv",
-    "tilu_csr_levels", "tilu_csr_residual_rows", "tilu_csr_tri_solve_blocks",
+    "tilu_csr_levels", "tilu_csr_residual_rows", "tilu_csr_tri_solve_blocks", "tilu_csr_matvec",
 )
 
 
@@ -106,6 +106,8 @@ def lib():
     L.tilu_mg_prolong_add.restype = _I
     L.tilu_dense_mv.argtypes = [_I, _P, _P, _P, _P]
     L.tilu_dense_mv.restype = _I
+    L.tilu_csr_matvec.argtypes = [_L, _P, _P, _P, _P, _P, _I, _P]
+    L.tilu_csr_matvec.restype = _I
     L.tilu_csr_levels.argtypes = [_I, _P, _P, _I, _P]
     L.tilu_csr_levels.restype = _I
     L.tilu_csr_residual_rows.argtypes = [_L, _P, _P, _P, _P, _P, _P, _P, _P]

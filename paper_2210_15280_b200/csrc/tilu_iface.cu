@@ -38,6 +38,21 @@ __global__ void __launch_bounds__(128) k_residual_rows(int64_t nrows, const int6
     r[i] = dsub(f[ids[i]], sum);
 }
 
+// y = M x (accumulate = 0) or y += M x (accumulate = 1) for a CSR matrix, one thread per row, the row's products
+// summed from 0 in index order (scipy's csr_matvec; for M = P^T stored as CSR that is csc_matvec's ascending
+// fine-index accumulation): the transfers of a macro-mesh hierarchy (Hierarchy.restrict / prolongate,
+// multigrid.py:377-388 with the caller's build_prolongation matrices).
+__global__ void __launch_bounds__(128) k_csr_matvec(int64_t nrows, const int64_t *__restrict__ indptr,
+                                                    const int64_t *__restrict__ indices, const double *__restrict__ data,
+                                                    const double *__restrict__ x, double *__restrict__ y, int accumulate)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    double sum = 0.0;
+    for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) sum = dadd(sum, dmul(data[k], x[indices[k]]));
+    y[i] = accumulate ? dadd(y[i], sum) : sum;
+}
+
 // One CTA per block.  Rows of block b: roff[b] .. roff[b+1]-1 of the concatenated block CSR (block-local
 // column indices).  Schedule: levels loff[b] .. loff[b+1]-1; level l holds rows perm[lptr[l] .. lptr[l+1]-1]
 // (block-local row numbers).  After the solve u[ids[row]] += z[row].
@@ -114,6 +129,21 @@ extern "C" int tilu_csr_residual_rows(int64_t nrows, const int64_t *indptr, cons
     abi_count_launches(1);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? TILU_OK : abi_fail(TILU_ECUDA, "csr_residual_rows: %s", cudaGetErrorString(e));
+}
+
+extern "C" int tilu_csr_matvec(int64_t nrows, const int64_t *indptr, const int64_t *indices, const double *data,
+                               const double *x, double *y, int accumulate, void *stream)
+{
+    if (nrows < 0 || (nrows > 0 && (!indptr || !indices || !data || !x || !y)))
+        return abi_fail(TILU_EINVAL, "csr_matvec: bad argument");
+    if (nrows == 0) return TILU_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    prof_begin(s);
+    iface::k_csr_matvec<<<(unsigned)((nrows + 127) / 128), 128, 0, s>>>(nrows, indptr, indices, data, x, y, accumulate);
+    prof_end("csr_matvec", s);
+    abi_count_launches(1);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TILU_OK : abi_fail(TILU_ECUDA, "csr_matvec: %s", cudaGetErrorString(e));
 }
 
 extern "C" int tilu_csr_tri_solve_blocks(int nblocks, const int64_t *roff, const int64_t *indptr, const int *indices,

@@ -153,3 +153,119 @@ class HybridSmoother:
         if self.symmetric:
             for kind in ("face", "edge", "vertex"):
                 self.interface_stage(u, f, kind, True)
+
+
+class _DevCSR:
+    """A scipy CSR matrix on the device (int64 indices, sorted) for tilu_csr_matvec / tilu_csr_residual_rows."""
+
+    def __init__(self, M, device):
+        M = M.tocsr()
+        M.sort_indices()
+        self.shape = M.shape
+        t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a, dtype=dt), device=device)  # noqa: E731
+        self.indptr, self.indices, self.data = t(M.indptr, np.int64), t(M.indices, np.int64), t(M.data, np.float64)
+
+    def matvec(self, x: torch.Tensor, y: torch.Tensor, accumulate: bool = False) -> torch.Tensor:
+        _lib.check(_lib.lib().tilu_csr_matvec(self.shape[0], self.indptr.data_ptr(), self.indices.data_ptr(),
+                                              self.data.data_ptr(), x.data_ptr(), y.data_ptr(), int(accumulate), _stream()))
+        return y
+
+
+class HybridHierarchy:
+    """Multigrid V-cycle on a macro-mesh whose tets share primitives: the reference ``Hierarchy`` (multigrid.py:
+    306-523) with every operation of the cycle on the device -- the hybrid smoother (interface stages + cell
+    stage), the residual with the assembled matrix, the transfers P e / P^T r with the caller's prolongation
+    matrices in scipy's accumulation order, and a dense solve on the coarsest level (the reference: PCG to
+    1e-12).  The mesh bookkeeping is the caller's (per level li: ``A[li]`` scipy CSR, ``P[li]`` from level li to
+    li + 1, ``prim_dofs[li]``, ``cell_dof[li]``, ``free[li]``), exactly the arrays the reference ``Hierarchy``
+    holds (``H.A``, ``H.P``, ``H.spaces[li].prim_dofs / cell_dof / free``)."""
+
+    def __init__(self, levels, A, P, prim_dofs, cell_dof, free, tets, coeff: CoefficientField | None = None,
+                 smoother: SmootherConfig | None = None, nu_pre: int = 3, nu_post: int = 3, symmetric: bool = True,
+                 fast: bool = False, factorize: str = "host", device="cuda"):
+        self.levels = [int(l) for l in levels]
+        nl = len(self.levels)
+        if not (len(A) == nl and len(P) == nl - 1 and len(prim_dofs) == nl and len(cell_dof) == nl and len(free) == nl):
+            raise ValueError("one A / prim_dofs / cell_dof / free per level and one P per level pair")
+        self.device = torch.device(device)
+        self.nu_pre, self.nu_post = int(nu_pre), int(nu_post)
+        self.ndof = [int(a.shape[0]) for a in A]
+        self.free = [torch.as_tensor(np.asarray(m, dtype=bool), device=self.device) for m in free]
+        self.smoothers = [None] + [HybridSmoother(A[li], prim_dofs[li], cell_dof[li], tets, self.levels[li], coeff,
+                                                  smoother, symmetric=symmetric, fast=fast, factorize=factorize,
+                                                  device=device) for li in range(1, nl)]
+        self.A = [None] + [_DevCSR(A[li], self.device) for li in range(1, nl)]
+        self._rows = [None] + [torch.arange(self.ndof[li], dtype=torch.int64, device=self.device) for li in range(1, nl)]
+        self.P = [_DevCSR(p, self.device) for p in P]
+        self.PT = [_DevCSR(p.T, self.device) for p in P]
+        f0 = np.nonzero(np.asarray(free[0], dtype=bool))[0]
+        A0 = A[0].tocsr()[np.ix_(f0, f0)].toarray()
+        self._coarse_idx = torch.as_tensor(f0, device=self.device)
+        self._coarse_inv = torch.as_tensor(np.linalg.inv(A0) if len(f0) else A0, device=self.device)
+        z = lambda li: torch.zeros(self.ndof[li], dtype=torch.float64, device=self.device)  # noqa: E731
+        self._r = [z(li) for li in range(nl)]
+        self._rc = [z(li) for li in range(nl)]
+        self._e = [z(li) for li in range(nl)]
+
+    @property
+    def top(self) -> int:
+        return len(self.levels) - 1
+
+    def zero(self, li: int) -> torch.Tensor:
+        return torch.zeros(self.ndof[li], dtype=torch.float64, device=self.device)
+
+    def smooth(self, li: int, u: torch.Tensor, f: torch.Tensor) -> None:
+        self.smoothers[li].smooth(u, f)
+
+    def residual(self, li: int, u: torch.Tensor, f: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """out = f - A u on free DoF, 0 elsewhere (multigrid.py:474-475)."""
+        a = self.A[li]
+        _lib.check(_lib.lib().tilu_csr_residual_rows(self.ndof[li], a.indptr.data_ptr(), a.indices.data_ptr(),
+                                                     a.data.data_ptr(), self._rows[li].data_ptr(), u.data_ptr(),
+                                                     f.data_ptr(), out.data_ptr(), _stream()))
+        out.masked_fill_(~self.free[li], 0.0)
+        return out
+
+    def coarse_solve(self, u: torch.Tensor, f: torch.Tensor) -> None:
+        m = self._coarse_idx.numel()
+        if m == 0:
+            return
+        b = f.index_select(0, self._coarse_idx).contiguous()
+        x = torch.empty_like(b)
+        _lib.check(_lib.lib().tilu_dense_mv(m, self._coarse_inv.data_ptr(), b.data_ptr(), x.data_ptr(), _stream()))
+        u.index_copy_(0, self._coarse_idx, x)
+
+    def v_cycle(self, li: int, u: torch.Tensor, f: torch.Tensor) -> None:
+        """In place on u (multigrid.py:459-485)."""
+        if li == 0:
+            self.coarse_solve(u, f)
+            return
+        for _ in range(self.nu_pre):
+            self.smooth(li, u, f)
+        r = self.residual(li, u, f, self._r[li])
+        rc = self.PT[li - 1].matvec(r, self._rc[li - 1])
+        rc.masked_fill_(~self.free[li - 1], 0.0)
+        ec = self._e[li - 1]
+        ec.zero_()
+        self.v_cycle(li - 1, ec, rc)
+        self.P[li - 1].matvec(ec, u, accumulate=True)
+        u.masked_fill_(~self.free[li], 0.0)
+        for _ in range(self.nu_post):
+            self.smooth(li, u, f)
+
+    def convergence_factor(self, steps: int = 20, seed: int = 42) -> float:
+        """Normalised power iteration on the error propagator, f = 0 (multigrid.py:505-523)."""
+        li = self.top
+        e0 = np.random.default_rng(seed).standard_normal(self.ndof[li])
+        e0[~self.free[li].cpu().numpy()] = 0.0
+        e0 /= np.linalg.norm(e0)
+        e = torch.as_tensor(e0, device=self.device)
+        f = self.zero(li)
+        rho = 0.0
+        for _ in range(steps):
+            self.v_cycle(li, e, f)
+            rho = float(torch.linalg.norm(e))
+            if not np.isfinite(rho) or rho == 0.0:
+                raise RuntimeError("power iteration collapsed")
+            e /= rho
+        return rho

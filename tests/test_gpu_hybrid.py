@@ -70,3 +70,42 @@ def test_cell_stage_and_smooth_vs_reference(name):
         H.smooth(u, f)
         assert float(np.abs(u.cpu().numpy() - ref).max() / np.abs(ref).max()) <= 1e-12
     assert not np.any(u.cpu().numpy()[~d["free"]])
+
+
+def test_hybrid_multigrid_v_cycle_vs_reference():
+    """V-cycles on the reference's cube_mesh (12 macro-tets, levels 2..4) with the hybrid smoother, transfers
+    with the reference's prolongation matrices: iterates and convergence factor vs Hierarchy.v_cycle /
+    convergence_factor.  The reference solves the coarsest level by PCG to 1e-12 |b| and multiplies by the
+    assembled matrix in the cell stage: agreement to 1e-10 relative (stated tolerance)."""
+    d = dict(np.load(os.path.join(GOLDEN, "hybrid_mg_L4.npz")))
+    top = load(str(d["top_from"]))
+    levels = [int(l) for l in d["levels"]]
+    nl = len(levels)
+
+    def csr(pfx, shape=None):
+        n = len(d[pfx + "_indptr"]) - 1
+        return sparse.csr_matrix((d[pfx + "_data"], d[pfx + "_indices"], d[pfx + "_indptr"]),
+                                 shape=shape or (n, n))
+
+    def prim(src, sfx):
+        return {k: [src[f"{k}{sfx}_ids"][a:b] for a, b in zip(src[f"{k}{sfx}_off"][:-1], src[f"{k}{sfx}_off"][1:])]
+                for k in ("vertex", "edge", "face")}
+
+    A = [csr(f"A{li}") for li in range(nl - 1)]
+    ntop = int(top["ndof"])
+    A.append(sparse.csr_matrix((top["data"], top["indices"], top["indptr"]), shape=(ntop, ntop)))
+    P = [csr(f"P{li}", tuple(int(v) for v in d[f"P{li}_shape"])) for li in range(nl - 1)]
+    prim_dofs = [prim(d, str(li)) for li in range(nl - 1)] + [prim(top, "")]
+    cell_dof = [d[f"cell_dof{li}"] for li in range(nl - 1)] + [top["cell_dof"]]
+    free = [d[f"free{li}"] for li in range(nl - 1)] + [top["free"]]
+    cfg = SmootherConfig(kind=str(d["kind"]), degrees=tuple(int(v) for v in d["degrees"]), variant=str(d["variant"]))
+    H = HY.HybridHierarchy(levels, A, P, prim_dofs, cell_dof, free, top["tets"], None, cfg, int(d["nu"]), int(d["nu"]),
+                           symmetric=bool(d["symmetric"]))
+    f = cuda(d["f"])
+    u = H.zero(H.top)
+    for k, ref in enumerate(d["u_cycles"]):
+        H.v_cycle(H.top, u, f)
+        err = float(np.abs(u.cpu().numpy() - ref).max() / np.abs(ref).max())
+        assert err <= 1e-10, (k, err)
+    rho = H.convergence_factor(steps=int(d["rho_steps"]), seed=42)
+    assert abs(rho - float(d["rho"])) <= 1e-8 * float(d["rho"]), (rho, float(d["rho"]))
