@@ -75,6 +75,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned &target)
 // (_kernels.py:52-57: beta / gamma are initialised neutral and only interior points are written)
 __device__ __forceinline__ double fv(const double *store, bool in, int64_t rank, int q)
 {
+    TILU_CHECK(!in || rank >= 0, "factor neighbour rank", rank, q);
     return in ? ld_rlx(store + 9 * rank + q) : (q == 7 ? 1.0 : 0.0);
 }
 
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(256) k_factor(const Args A, const int *__restr
             if (x < 1 || x > xe) continue;
             const int64_t base = row_offset(n, z, y);
             const int64_t rank = base + x;
+            TILU_CHECK(rank > 0 && rank < num_points(n) && y >= 1 && z >= 1 && y + z <= n - 2, "factor point", rank, t);
             double a[15];
             if (A.amode == 2) {
                 const int T4 = 4 * n + 1;
@@ -191,6 +193,7 @@ __global__ void k_gather_rows(const double *__restrict__ store, const int64_t *_
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count * 9) return;
+    TILU_CHECK(ranks[i / 9] >= 0, "gather rank", ranks[i / 9], i);
     out[i] = store[9 * ranks[i / 9] + i % 9];
 }
 

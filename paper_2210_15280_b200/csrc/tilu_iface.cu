@@ -70,8 +70,10 @@ __global__ void __launch_bounds__(128) k_tri_solve_blocks(const int64_t *__restr
         for (int64_t q = lptr[l] + threadIdx.x; q < lptr[l + 1]; q += blockDim.x) {
             const int i = perm[q];
             double acc = b[r0 + i], diag = 0.0;
+            TILU_CHECK(i >= 0 && i < m, "tri solve row", i, blk);
             for (int64_t k = indptr[r0 + i]; k < indptr[r0 + i + 1]; ++k) {
                 const int j = indices[k];
+                TILU_CHECK(j >= 0 && j < m, "tri solve column", j, blk);
                 if (upper ? (j > i) : (j < i)) acc = dsub(acc, dmul(data[k], zb[j]));
                 else if (j == i) diag = data[k];
             }

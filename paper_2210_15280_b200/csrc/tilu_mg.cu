@@ -45,6 +45,8 @@ __global__ void __launch_bounds__(128) k_restrict(int nc, const double *__restri
 #pragma unroll
             for (int d = 0; d < 15; ++d) {
                 const int dx = kOff[d][0], dy = kOff[d][1], dz = kOff[d][2];
+                TILU_CHECK(2 * xc + dx >= 0 && 2 * yc + dy >= 0 && 2 * zc + dz >= 0 &&
+                               2 * (xc + yc + zc) + dx + dy + dz <= nf, "restrict fine point", xc, d);
                 const double v = rf[rank_of(nf, 2 * xc + dx, 2 * yc + dy, 2 * zc + dz)];
                 acc = dadd(acc, (dx | dy | dz) ? dmul(0.5, v) : v);
             }
@@ -79,6 +81,8 @@ __global__ void __launch_bounds__(128) k_prolong_add(int nc, const double *__res
             default: ax = -1, ay = 1, az = -1; break;
             }
             const int hx = (xf + ax) >> 1, hy = (yf + ay) >> 1, hz = (zf + az) >> 1;
+            TILU_CHECK(hx >= 0 && hy >= 0 && hz >= 0 && hx + hy + hz <= nc && hx - ax >= 0 && hy - ay >= 0 && hz - az >= 0 &&
+                           hx + hy + hz - ax - ay - az <= nc, "prolong coarse endpoints", xf, code);
             const double ea = ec[rank_of(nc, hx, hy, hz)];
             const double eb = ec[rank_of(nc, hx - ax, hy - ay, hz - az)];
             add = dadd(dmul(0.5, ea), dmul(0.5, eb));
