@@ -79,9 +79,13 @@ class SweepNorms:
             self.side.wait_event(ev)
             allreduce_norms(self.norms[k:k + 1], self.group)
 
-    def result(self) -> "torch.Tensor":
+    def result(self, check_finite: bool = False) -> "torch.Tensor":
+        """The allreduced per-sweep norms; ``check_finite`` (synchronises) raises FloatingPointError on NaN / inf."""
         if self.side is not None:
             torch.cuda.current_stream(self.norms.device).wait_stream(self.side)
+        if check_finite and not bool(torch.isfinite(self.norms).all()):
+            k = int(torch.nonzero(~torch.isfinite(self.norms))[0])
+            raise FloatingPointError(f"non-finite global residual norm before sweep {k}")
         return self.norms
 
 

@@ -404,9 +404,12 @@ class SurrogateILUSmoother:
     def residual(self, u, f, w=None, norms: bool = False):
         return self.plan.residual(u, f, w, norms)
 
-    def apply(self, u, f, sweeps: int = 1, *, residual_norms: bool = False):
+    def apply(self, u, f, sweeps: int = 1, *, residual_norms: bool = False, check_finite: bool = False):
         """In place on u (CUDA fp64 [grid] or [ntets, grid] sharing this operator).
-        Returns ||f - A u||^2 before each sweep ([sweeps, ntets]) if ``residual_norms``."""
+        Returns ||f - A u||^2 before each sweep ([sweeps, ntets]) if ``residual_norms``.
+        ``check_finite`` (implies the norms; synchronises the stream): raise FloatingPointError when a
+        residual norm is NaN or infinite -- a diverged or corrupted iterate is reported, not propagated."""
+        residual_norms = residual_norms or check_finite
         host = isinstance(u, np.ndarray)
         if host:
             ut = torch.as_tensor(np.ascontiguousarray(u), device="cuda")
@@ -414,10 +417,13 @@ class SurrogateILUSmoother:
         else:
             ut, ft = u, f
         rn = self.plan.sweep(ut, ft, sweeps, norms=residual_norms, stored=self._stored)
+        if check_finite and not bool(torch.isfinite(rn).all()):
+            bad = torch.nonzero(~torch.isfinite(rn))[0].tolist()
+            raise FloatingPointError(f"non-finite residual norm before sweep {bad[0]} (tet {bad[1]})")
         if host:
             u[...] = ut.cpu().numpy()
             rn = None if rn is None else rn.cpu().numpy()
         return rn
 
-    def apply_many(self, us, fs, sweeps: int = 1, *, residual_norms: bool = False):
-        return self.apply(us, fs, sweeps, residual_norms=residual_norms)
+    def apply_many(self, us, fs, sweeps: int = 1, *, residual_norms: bool = False, check_finite: bool = False):
+        return self.apply(us, fs, sweeps, residual_norms=residual_norms, check_finite=check_finite)

@@ -188,3 +188,15 @@ def test_boundary_values_are_read_as_given(level, sched, ntets):
     u = cuda(z0)
     p.sweep(u, cuda(f), 1)
     assert np.array_equal(u.cpu().numpy(), ref0)
+
+
+def test_check_finite_reports_a_corrupted_iterate():
+    level = 5
+    sm = SurrogateILUSmoother.setup(lattice.unit_tet(), level, (3, 3, 3))
+    u = cuda(u0_of(level)[0])
+    f = torch.zeros_like(u)
+    rn = sm.apply(u, f, 2, check_finite=True)
+    assert rn.shape == (2, 1)
+    u[int(np.nonzero(lattice.interior_mask(level))[0][100])] = float("nan")
+    with pytest.raises(FloatingPointError):
+        sm.apply(u, f, 1, check_finite=True)

@@ -176,3 +176,15 @@ def test_macro_mesh_norm_aggregation_gloo_world2():
     assert np.array_equal(g0, g1)                     # every rank holds the same global norms
     np.testing.assert_allclose(g0, want, rtol=1e-14)  # = sum over all 384 tets' norms
     assert np.all(np.diff(g0) < 0)                     # the smoother decreases the residual
+
+
+def test_sweep_norms_check_finite_cpu():
+    import torch
+
+    from paper_2210_15280_b200.partition import SweepNorms
+    agg = SweepNorms(2, torch.device("cpu"))
+    agg.add(0, torch.tensor([1.0, 2.0], dtype=torch.float64))
+    agg.add(1, torch.tensor([float("nan"), 2.0], dtype=torch.float64))
+    assert float(agg.result()[0]) == 3.0
+    with pytest.raises(FloatingPointError):
+        agg.result(check_finite=True)
