@@ -28,6 +28,7 @@
 // Every load of point x+1 is issued while point x computes (one-point software prefetch).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -220,6 +221,27 @@ __device__ __forceinline__ void ready(Vt<T> &v, const double *p)
     while (__any_sync(0xffffffffu, any_sent(v))) {
         __nanosleep(32);
         v = ldcgv<T>(p);
+        if (++spins > (1ll << 26)) __trap();
+    }
+#ifdef TILU_STATS
+    if ((threadIdx.x & 31) == 0 && spins) atomicAdd(&g_stats[2], (unsigned long long)spins);
+#endif
+}
+
+// Three neighbour values at once: every value still pending is re-read in the same iteration (the loads go out
+// back to back: one L2 round trip per iteration for all of them, not one loop per value).
+template <int T>
+__device__ __forceinline__ void ready3(Vt<T> &a, const double *pa, Vt<T> &b, const double *pb, Vt<T> &c, const double *pc)
+{
+    long long spins = 0;
+    for (;;) {
+        const bool ra = __any_sync(0xffffffffu, any_sent(a)), rb = __any_sync(0xffffffffu, any_sent(b)),
+                   rc = __any_sync(0xffffffffu, any_sent(c));
+        if (!(ra | rb | rc)) break;
+        __nanosleep(32);
+        if (ra) a = ldcgv<T>(pa);
+        if (rb) b = ldcgv<T>(pb);
+        if (rc) c = ldcgv<T>(pc);
         if (++spins > (1ll << 26)) __trap();
     }
 #ifdef TILU_STATS
@@ -531,6 +553,8 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? TILU_FWD_M
             TILU_STAT(0, 1);
             if (__any_sync(0xffffffffu, any_sent(cw.s) | any_sent(cw.bn) | any_sent(cw.bc))) {
                 TILU_STAT(1, 1);
+                // (one loop per value: the joint loop ready3 of the backward kernel costs the forward kernel
+                // registers -- measured 1.45 -> 1.58 ms)
                 ready<T>(cw.s, wa + R.os + X + GW);
                 ready<T>(cw.bn, wa + R.obn + X);
                 ready<T>(cw.bc, wa + R.obc + X + GW);
@@ -802,9 +826,7 @@ __global__ void __launch_bounds__(kWarps * 32, T == 1 ? 5 : (T == 2 ? TILU_BWD_M
             TILU_STAT(0, 1);
             if (__any_sync(0xffffffffu, any_sent(cw.n) | any_sent(cw.ts) | any_sent(cw.tc))) {
                 TILU_STAT(1, 1);
-                ready<T>(cw.n, wb + R.on + X - GW);
-                ready<T>(cw.ts, wb + R.ots + X);
-                ready<T>(cw.tc, wb + R.otc + X - GW);
+                ready3<T>(cw.n, wb + R.on + X - GW, cw.ts, wb + R.ots + X, cw.tc, wb + R.otc + X - GW);
             }
             const Vt<T> &wn = cw.n, &wts = cw.ts, &wtc = cw.tc;
             const double inv_d = L[7];
@@ -1074,13 +1096,13 @@ void launch_arm(const PlanDev &P, double *wa, const unsigned long long *hdr, uns
 
 // Persistent grid: as many CTAs as fit on the device at once (queried once per kernel).
 template <class Kern>
-static unsigned persistent_grid(Kern k, size_t smem);
+static unsigned persistent_grid(Kern k, size_t smem, int cap);
 
 // Launch a persistent batched kernel.  Its dynamic shared-memory attribute and resident grid are
 // cached per KERNEL and per device ordinal (a map keyed by the kernel's address: kernels of one
 // signature share a C++ type, so a per-type static would skip the attribute of the second one).
 template <class Kern>
-static void launch_persistent(Kern kern, size_t sm, const PlanDev &P, BatchArgs A, cudaStream_t s)
+static void launch_persistent(Kern kern, size_t sm, const PlanDev &P, BatchArgs A, cudaStream_t s, int cap = 0)
 {
     static std::mutex mu;
     static std::map<std::pair<const void *, int>, unsigned> grids;
@@ -1091,21 +1113,24 @@ static void launch_persistent(Kern kern, size_t sm, const PlanDev &P, BatchArgs 
         std::lock_guard<std::mutex> lk(mu);
         auto key = std::make_pair(reinterpret_cast<const void *>(kern), dev);
         auto it = grids.find(key);
-        if (it == grids.end()) it = grids.emplace(key, persistent_grid(kern, sm)).first;
+        if (it == grids.end()) it = grids.emplace(key, persistent_grid(kern, sm, cap)).first;
         grid = it->second;
     }
     A.nwarps = (int)grid * kWarps;
     kern<<<grid, kWarps * 32, sm, s>>>(P, A);
 }
 
+// cap > 0: at most that many CTAs per SM (the passes are dependency-bound: beyond a point more resident
+// warps only add rows that spin on sentinels)
 template <class Kern>
-static unsigned persistent_grid(Kern k, size_t smem)
+static unsigned persistent_grid(Kern k, size_t smem, int cap)
 {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kWarps * 32, smem);
+    if (cap > 0) per = std::min(per, cap);
     return (unsigned)std::max(1, sms * std::max(per, 1));
 }
 
@@ -1113,7 +1138,8 @@ template <int K, int T, bool TAB>
 static void launch_fwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_t s)
 {
     constexpr size_t sm = ring_smem<kFwdNS, T, kStagesF, kChunkF>();
-    auto run = [&](auto kern) { launch_persistent<decltype(kern)>(kern, sm, P, A, s); };
+    static const int cap = std::getenv("TILU_FWD_CTAS") ? std::atoi(std::getenv("TILU_FWD_CTAS")) : 0;
+    auto run = [&](auto kern) { launch_persistent<decltype(kern)>(kern, sm, P, A, s, cap); };
     const int am = P.seedA ? 3 : P.arow ? 1 : 0;
     if (exact) {
         if (am == 3) run(k_batch_fwd<K, true, 3, T, TAB>);
@@ -1130,7 +1156,8 @@ template <int K, int T, bool TAB>
 static void launch_bwd_kt(const PlanDev &P, BatchArgs A, bool exact, cudaStream_t s)
 {
     constexpr size_t sm = ring_smem<kBwdNS, T, kStages<T>>();
-    auto run = [&](auto kern) { launch_persistent<decltype(kern)>(kern, sm, P, A, s); };
+    static const int cap = std::getenv("TILU_BWD_CTAS") ? std::atoi(std::getenv("TILU_BWD_CTAS")) : 0;
+    auto run = [&](auto kern) { launch_persistent<decltype(kern)>(kern, sm, P, A, s, cap); };
     if (exact) run(k_batch_bwd<K, true, T, TAB>);
     else run(k_batch_bwd<K, false, T, TAB>);
 }
