@@ -38,6 +38,9 @@
 
 namespace tilu {
 
+#ifndef TILU_POLL_NS
+#define TILU_POLL_NS 32   // back-off between re-reads of a value that is still the sentinel
+#endif
 #ifndef TILU_BWD_MINB2
 #define TILU_BWD_MINB2 3   // resident CTAs per SM the backward kernel (2 tets per lane) is compiled for
 #endif
@@ -219,7 +222,7 @@ __device__ __forceinline__ void ready(Vt<T> &v, const double *p)
 {
     long long spins = 0;
     while (__any_sync(0xffffffffu, any_sent(v))) {
-        __nanosleep(32);
+        __nanosleep(TILU_POLL_NS);
         v = ldcgv<T>(p);
         if (++spins > (1ll << 26)) __trap();
     }
@@ -238,7 +241,7 @@ __device__ __forceinline__ void ready3(Vt<T> &a, const double *pa, Vt<T> &b, con
         const bool ra = __any_sync(0xffffffffu, any_sent(a)), rb = __any_sync(0xffffffffu, any_sent(b)),
                    rc = __any_sync(0xffffffffu, any_sent(c));
         if (!(ra | rb | rc)) break;
-        __nanosleep(32);
+        __nanosleep(TILU_POLL_NS);
         if (ra) a = ldcgv<T>(pa);
         if (rb) b = ldcgv<T>(pb);
         if (rc) c = ldcgv<T>(pc);
