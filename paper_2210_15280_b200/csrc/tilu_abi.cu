@@ -180,6 +180,9 @@ int batch_tpl(int ntets)
 {
     static const char *e = std::getenv("TILU_TPL");
     if (e && (e[0] == '1' || e[0] == '2')) return e[0] - '0';
+    // 65..96 tets: three full 32-lane groups beat one full + one half-empty 64-lane group (tools/tets_scan.py:
+    // 1.46 vs 1.57 ms per sweep at level 7)
+    if (ntets > 64 && ntets <= 96) return 1;
     return ntets > 32 ? 2 : 1;
 }
 

@@ -200,3 +200,23 @@ def test_check_finite_reports_a_corrupted_iterate():
     u[int(np.nonzero(lattice.interior_mask(level))[0][100])] = float("nan")
     with pytest.raises(FloatingPointError):
         sm.apply(u, f, 1, check_finite=True)
+
+
+@pytest.mark.parametrize("ntets", [33, 70, 96, 97])
+def test_batch_group_shapes_bitwise(ntets):
+    """Tets-per-lane selection (one tet per lane up to 32 and for 65..96 tets, two otherwise): partly filled
+    groups and both group widths give the oracle's result for every tet."""
+    level = 4
+    src = S.stencil_source(lattice.kuhn_tet((0, 1, 2)), level, S.CoefficientField.constant(1.0))
+    fit = F.fit_surrogate_ilu(src, level, (3, 3, 3), "v1")
+    p = DevicePlan(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows, arow=src.data)
+    u0 = u0_of(level, ntets, seed=ntets)
+    f = np.zeros_like(u0)
+    u = cuda(u0)
+    p.sweep(u, cuda(f), 2)
+    got = u.cpu().numpy()
+    sur = O.OracleSurrogate(level, fit.lcoefs, fit.dcoefs, "v1", fit.band_ranks, fit.store_rows)
+    for t in (0, 31, 32, ntets - 1):
+        ref = u0[t].copy()
+        O.sweeps(sur, level, src.data, ref, f[t], 2)
+        assert np.array_equal(got[t], ref), t
