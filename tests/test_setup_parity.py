@@ -91,3 +91,25 @@ def test_unknown_variant():
     src = S.stencil_source(lattice.unit_tet(), 3, S.CoefficientField.constant(1.0))
     with pytest.raises(ValueError):
         F.fit_surrogate_ilu(src, 3, (1, 1, 1), "v3")
+
+
+@pytest.mark.parametrize("name,coeff", [("fit_kuhn_L7_q6", lambda: S.CoefficientField.constant(1.0)),
+                                        ("fit_cfg5_L8_q4", lambda: S.diag_tensor((1, 1e-2, 1)))])
+def test_surrogate_fit_bitwise_at_benchmark_levels(name, coeff):
+    """P2 at config 4's level 7 (Kuhn tet, q = 6) and config 5's level 8 (q = 4): this repo's setup
+    (rows, native factorization, sampling, LSQ fit, degree degrade) reproduces the reference's
+    build_surrogate_ilu arrays bit for bit (fixtures from the live reference, tests/golden/make_fit_large.py)."""
+    import hashlib
+
+    d = load(name)
+    L, q = int(d["level"]), int(d["q"])
+    src = S.stencil_source(d["verts"], L, coeff())
+    fit = F.fit_surrogate_ilu(src, L, (q, q, q), "v1")
+    assert tuple(fit.degrees) == tuple(int(v) for v in d["eff_degrees"])
+    assert fit.stride == int(d["stride"])
+    assert np.array_equal(fit.lcoefs, d["lcoefs"])
+    assert np.array_equal(fit.dcoefs, d["dcoefs"])
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    assert len(fit.band_ranks) == int(d["nband"])
+    assert sha(fit.band_ranks) == str(d["band_sha"])
+    assert sha(fit.store_rows) == str(d["store_sha"])
