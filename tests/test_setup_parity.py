@@ -113,3 +113,22 @@ def test_surrogate_fit_bitwise_at_benchmark_levels(name, coeff):
     assert len(fit.band_ranks) == int(d["nband"])
     assert sha(fit.band_ranks) == str(d["band_sha"])
     assert sha(fit.store_rows) == str(d["store_sha"])
+
+
+def test_config3_level9_setup_equals_the_reference():
+    """P2 at the north star's size: the arrays this repo's setup produced for config 3 at level 9 (stored in
+    l9_config3.npz, the fixture the GPU parity test and the bench's config-3 leg are pinned to) against the
+    UNMODIFIED reference's own 30-minute setup (stencil_source + build_surrogate_ilu,
+    tests/golden/make_fit_l9_reference.py): fitted coefficients bit for bit, per-point operator rows, band ranks
+    and the V1 band store by SHA-256."""
+    ref_path = os.path.join(GOLDEN, "fit_cfg3_L9_ref.npz")
+    if not os.path.exists(ref_path):
+        pytest.skip("reference level-9 setup fixture not generated")
+    ref, ours = np.load(ref_path), np.load(os.path.join(GOLDEN, "l9_config3.npz"))
+    assert tuple(int(v) for v in ours["eff_degrees"]) == tuple(int(v) for v in ref["eff_degrees"])
+    assert int(ours["stride"]) == int(ref["stride"])
+    assert np.array_equal(ours["lcoefs"], ref["lcoefs"])
+    assert np.array_equal(ours["dcoefs"], ref["dcoefs"])
+    assert str(ours["rows_sha"]) == str(ref["rows_sha"])
+    assert str(ours["band_ranks_sha"]) == str(ref["band_sha"])
+    assert str(ours["band_sha"]) == str(ref["store_sha"])
