@@ -108,3 +108,23 @@ def test_many_tets_openmp_equals_serial():
     used = O.sweeps_many(sur, L, d["arows"][0], us, fs, 2, nthreads=2)
     assert used >= 1
     assert np.array_equal(us, ref)
+
+
+def test_level9_oracle_run_equals_the_reference_kernels():
+    """The level-9 config-3 fixture (the C oracle's 100 sweeps: what the GPU parity test and the bench's config-3
+    leg are pinned to) against the REFERENCE's own Numba kernels run on the same arrays
+    (tests/golden/make_l9_reference_sweeps.py): SHA-256 of the full 22.6M-entry iterate after every stored sweep."""
+    import os
+
+    import numpy as np
+    import pytest
+
+    from conftest import GOLDEN
+    path = os.path.join(GOLDEN, "l9_reference_sweeps.npz")
+    if not os.path.exists(path):
+        pytest.skip("reference level-9 sweep fixture not generated")
+    ref, ours = np.load(path), np.load(os.path.join(GOLDEN, "l9_config3.npz"))
+    mine = {int(k): str(h) for k, h in zip(ours["snaps"], ours["u_sha"])}
+    assert len(ref["snaps"]) >= 3
+    for k, h in zip(ref["snaps"], ref["u_sha"]):
+        assert mine[int(k)] == str(h), f"sweep {int(k)}"
