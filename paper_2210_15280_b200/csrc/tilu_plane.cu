@@ -1370,6 +1370,19 @@ void plane_free(void *ws)
 
 int64_t plane_interior_points(const tilu_plan *p) { return p->interior; }
 
+// The workspace's "last call finished" event, usable inside a stream capture (CUDA graph of a multigrid
+// cycle): there the wait / record become external event nodes; outside a capture the plain calls.
+static bool capturing(cudaStream_t s)
+{
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive;
+}
+static void ws_wait(cudaEvent_t e, cudaStream_t s) { cudaStreamWaitEvent(s, e, capturing(s) ? cudaEventWaitExternal : 0); }
+static void ws_record(cudaEvent_t e, cudaStream_t s)
+{
+    cudaEventRecordWithFlags(e, s, capturing(s) ? cudaEventRecordExternal : 0);
+}
+
 // `sweeps` smoothing steps on one macro-tet in the reference layout: pack, sweeps, unpack.
 int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int sweeps, double *rnorm2,
                 cudaStream_t s, int *launches, bool stored)
@@ -1388,7 +1401,7 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
         p->plane = nw;
     }
     Workspace *w = static_cast<Workspace *>(p->plane);
-    cudaStreamWaitEvent(s, w->done, 0);
+    ws_wait(w->done, s);
     const PlanDev &P = p->dev;
     int nl = 0;
     int rc = TILU_OK;
@@ -1451,7 +1464,7 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
         if (dbg && dbg[0] == '1') {
             launch_xpose(P, w->g, w->W, u, true, s);
             w->armed = false;
-            cudaEventRecord(w->done, s);
+            ws_record(w->done, s);
             return ok ? TILU_OK : TILU_EUNSUPPORTED;
         }
         prof_begin(s);
@@ -1509,7 +1522,7 @@ int plane_sweep(const tilu_plan *cp, double *u, const double *f, int ntets, int 
         rc = TILU_ECUDA;
         w->armed = false;
     }
-    cudaEventRecord(w->done, s);
+    ws_record(w->done, s);
     if (launches) *launches += nl;
     return rc;
 }
