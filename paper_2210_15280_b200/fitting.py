@@ -265,6 +265,8 @@ def factorize_tet_device(source: StencilSource, level: int, *, full_store: bool 
             data = source.data
             rows_dev = (data if isinstance(data, torch.Tensor) else
                         torch.as_tensor(np.ascontiguousarray(data, dtype=np.float64), device=dev)).contiguous()
+            if tuple(rows_dev.shape) != (grid, 15) or rows_dev.dtype != torch.float64 or not rows_dev.is_cuda:
+                raise ValueError(f"per-point operator rows must be float64 [{grid}, 15] on the device")
         rc = L.tilu_factorize_device(
             level, rows_dev.data_ptr() if rows_dev is not None else None,
             arow.ctypes.data if arow is not None else None,

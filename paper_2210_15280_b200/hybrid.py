@@ -31,6 +31,16 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def _check_vec(name: str, v, n: int, device) -> None:
+    """The kernels index the vectors with the mesh's global ids: wrong sizes / dtypes / devices must fail here,
+    not read past an allocation."""
+    if not (isinstance(v, torch.Tensor) and v.is_cuda and v.dtype == torch.float64 and v.is_contiguous()
+            and v.dim() == 1 and v.numel() == n):
+        raise ValueError(f"{name} must be a contiguous CUDA float64 vector of {n} entries")
+    if v.device != torch.device(device) and torch.device(device).index is not None:
+        raise ValueError(f"{name} is on {v.device}, the smoother on {device}")
+
+
 def _schedule(blocks, upper: bool):
     """Level schedule of every block: (loff [nb+1], lptr [nlev+1], perm [nrows])."""
     L = _lib.lib()
@@ -110,6 +120,9 @@ class HybridSmoother:
         self.level = int(level)
         self.symmetric = bool(symmetric)
         self.device = torch.device(device)
+        self.ndof = int(A.shape[0])
+        if A.shape[0] != A.shape[1]:
+            raise ValueError("A must be square")
         self.config = config if config is not None else SmootherConfig()
         coeff = coeff if coeff is not None else CoefficientField.constant(1.0)
         self.stages = {k: InterfaceStage(A, [np.asarray(i) for i in prim_dofs.get(k, [])], device)
@@ -118,6 +131,13 @@ class HybridSmoother:
         grid = lattice.grid_size(level)
         if cell_dof.ndim != 2 or cell_dof.shape[1] != grid:
             raise ValueError(f"cell_dof must be [ntets, {grid}]")
+        if cell_dof.size and (cell_dof.min() < 0 or cell_dof.max() >= self.ndof):
+            raise ValueError("cell_dof holds ids outside the matrix")
+        for k in ("vertex", "edge", "face"):
+            for ids in prim_dofs.get(k, []):
+                ids = np.asarray(ids)
+                if ids.size and (ids.min() < 0 or ids.max() >= self.ndof):
+                    raise ValueError(f"{k} primitive holds ids outside the matrix")
         self.ntets = cell_dof.shape[0]
         sources = [stencil_source(np.asarray(t, dtype=np.float64), level, coeff) for t in tets]
         if len(sources) != self.ntets:
@@ -132,11 +152,15 @@ class HybridSmoother:
         self._imask = torch.as_tensor(imask, device=self.device)
 
     def interface_stage(self, u, f, kind: str, transposed: bool = False) -> None:
+        _check_vec("u", u, self.ndof, self.device)
+        _check_vec("f", f, self.ndof, self.device)
         self.stages[kind].apply(u, f, transposed)
 
     def cell_stage(self, u: torch.Tensor, f: torch.Tensor) -> None:
         """Every macro-tet interior: u_t += M_t^{-1} (f - A u)_t with the tet's boundary values taken from
         the global vector (multigrid.py:414-429).  All tets read the same u (block Jacobi across cells)."""
+        _check_vec("u", u, self.ndof, self.device)
+        _check_vec("f", f, self.ndof, self.device)
         locs = []
         for sm, gidx in zip(self.smoothers, self._gather):
             ul = u[gidx].contiguous()
@@ -237,6 +261,8 @@ class HybridHierarchy:
 
     def v_cycle(self, li: int, u: torch.Tensor, f: torch.Tensor) -> None:
         """In place on u (multigrid.py:459-485)."""
+        _check_vec("u", u, self.ndof[li], self.device)
+        _check_vec("f", f, self.ndof[li], self.device)
         if li == 0:
             self.coarse_solve(u, f)
             return

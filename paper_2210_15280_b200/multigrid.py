@@ -199,6 +199,8 @@ def schur_inner_solve(hier: Hierarchy, rhs: torch.Tensor, tol: float = 1e-8, max
     interior DoF in lattice-rank order; returns the interior solution (CUDA tensors).  Raises
     InnerSolveError when the residual stays above 10 tol |f| (schur.py:96-99)."""
     lvl = hier.levels[hier.top]
+    if rhs.dim() != 1 or rhs.numel() != lattice.interior_size(lvl):
+        raise ValueError(f"rhs must hold the {lattice.interior_size(lvl)} interior DoF of level {lvl}")
     idx = torch.as_tensor(lattice.lattice_rank(lattice.lattice_coords(lvl, "interior"), lvl), device=hier.device)
     f = hier.zero(hier.top)
     f.index_copy_(0, idx, rhs.to(hier.device, torch.float64))

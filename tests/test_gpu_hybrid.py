@@ -109,3 +109,21 @@ def test_hybrid_multigrid_v_cycle_vs_reference():
         assert err <= 1e-10, (k, err)
     rho = H.convergence_factor(steps=int(d["rho_steps"]), seed=42)
     assert abs(rho - float(d["rho"])) <= 1e-8 * float(d["rho"]), (rho, float(d["rho"]))
+
+
+def test_hybrid_smoother_rejects_wrong_vectors():
+    d = load("hybrid_L3_surrogate_ilu")
+    H = build(d)
+    u, f = cuda(d["u0"]), cuda(d["f"])
+    with pytest.raises(ValueError):
+        H.smooth(u[:-1].contiguous(), f)
+    with pytest.raises(ValueError):
+        H.smooth(u.float(), f)
+    with pytest.raises(ValueError):
+        H.smooth(u, torch.as_tensor(d["f"]))          # host tensor
+    n = int(d["ndof"])
+    A = sparse.csr_matrix((d["data"], d["indices"], d["indptr"]), shape=(n, n))
+    bad = d["cell_dof"].copy()
+    bad[0, 0] = n
+    with pytest.raises(ValueError):
+        HY.HybridSmoother(A, {}, bad, d["tets"], int(d["level"]))
